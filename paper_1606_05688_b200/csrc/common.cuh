@@ -1,0 +1,161 @@
+// Shared host/device plumbing of the vxg library: error types that map onto
+// the C-ABI status codes, the per-GPU context (stream + budgeted
+// stream-ordered allocator = the device MemoryTracker of
+// proj/include/voxin/memory.hpp:15-51 with byte units), and launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "vxg.h"
+
+namespace vxg {
+
+using i64 = int64_t;
+
+struct invalid : std::invalid_argument {
+  explicit invalid(const std::string& w) : std::invalid_argument(w) {}
+};
+struct exhausted : std::runtime_error {
+  explicit exhausted(const std::string& w) : std::runtime_error(w) {}
+};
+struct cuda_failure : std::runtime_error {
+  explicit cuda_failure(const std::string& w) : std::runtime_error(w) {}
+};
+struct parse_failure : std::runtime_error {
+  explicit parse_failure(const std::string& w) : std::runtime_error(w) {}
+};
+
+inline void require(bool cond, const char* what) {
+  if (!cond) throw invalid(what);
+}
+
+#define VXG_CUDA_CHECK(expr)                                                             \
+  do {                                                                                   \
+    cudaError_t e__ = (expr);                                                            \
+    if (e__ != cudaSuccess)                                                              \
+      throw ::vxg::cuda_failure(std::string(#expr) + ": " + cudaGetErrorString(e__));    \
+  } while (0)
+
+struct V3 {
+  i64 x = 1, y = 1, z = 1;
+  i64 operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+  i64& operator[](int a) { return a == 0 ? x : (a == 1 ? y : z); }
+  i64 vol() const { return x * y * z; }
+  bool positive() const { return x > 0 && y > 0 && z > 0; }
+  bool operator==(const V3& o) const { return x == o.x && y == o.y && z == o.z; }
+  static V3 of(const int64_t* a) { return V3{a[0], a[1], a[2]}; }
+  static V3 cube(i64 e) { return V3{e, e, e}; }
+};
+
+// One context per GPU.  All work is issued on `stream`; allocations are
+// stream-ordered (cudaMallocAsync) and charged against `budget` bytes.
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  i64 budget = 0;
+  i64 current = 0;
+  i64 peak = 0;
+  int num_sms = 148;
+  int* d_flag = nullptr;  // device error flag (NaN seen by pools)
+  std::atomic<i64> launches{0};
+  std::mutex mu;
+
+  void charge(i64 bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (current + bytes > budget)
+      throw exhausted("HBM budget exceeded: need " + std::to_string(current + bytes) +
+                      " bytes, budget " + std::to_string(budget));
+    current += bytes;
+    if (current > peak) peak = current;
+  }
+  void release(i64 bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    current -= bytes;
+  }
+  void counted(i64 n = 1) { launches += n; }
+};
+
+// RAII device buffer charged against the context budget.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(Ctx* c, i64 bytes) { alloc(c, bytes); }
+  ~DevBuf() { reset(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : c_(o.c_), p_(o.p_), n_(o.n_) { o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      c_ = o.c_; p_ = o.p_; n_ = o.n_;
+      o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(Ctx* c, i64 bytes) {
+    reset();
+    if (bytes <= 0) return;
+    c->charge(bytes);
+    void* p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
+    if (e != cudaSuccess) {
+      c->release(bytes);
+      cudaGetLastError();
+      if (e == cudaErrorMemoryAllocation)
+        throw exhausted("device allocation of " + std::to_string(bytes) + " bytes failed");
+      throw cuda_failure(std::string("cudaMallocFromPoolAsync: ") + cudaGetErrorString(e));
+    }
+    c_ = c; p_ = p; n_ = bytes;
+  }
+  void reset() {
+    if (p_) {
+      cudaFreeAsync(p_, c_->stream);
+      c_->release(n_);
+    }
+    c_ = nullptr; p_ = nullptr; n_ = 0;
+  }
+  template <class T = float>
+  T* as() const { return static_cast<T*>(p_); }
+  void* get() const { return p_; }
+  i64 bytes() const { return n_; }
+
+ private:
+  Ctx* c_ = nullptr;
+  void* p_ = nullptr;
+  i64 n_ = 0;
+};
+
+inline unsigned grid_for(i64 n, int block, i64 cap = (i64(1) << 31) - 1) {
+  i64 g = (n + block - 1) / block;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw cuda_failure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- kernel entry points (implemented in the k_*.cu units) -----------------
+
+// pools (k_pool.cu)
+void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 b0, i64 nb);
+void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out);
+void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
+                      const i64* windows, int nwin, float* dense, i64 S0);
+void launch_nan_check(Ctx* c, const float* x, i64 count);
+bool read_and_clear_flag(Ctx* c);
+
+// direct convolution (k_direct.cu)
+void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float* w, i64 fo,
+                        V3 k, const float* bias, bool relu, float* out);
+
+}  // namespace vxg

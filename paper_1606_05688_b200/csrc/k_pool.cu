@@ -1,0 +1,208 @@
+// K6 / K7: max-pooling fragments (MPF), plain max pooling and fragment
+// recombination.  All HBM-bound data movement: one read of the input and one
+// write of the output per element.
+//
+//   mpf_pool            proj/include/voxin/layers.hpp:424-470
+//   max_pool            proj/include/voxin/layers.hpp:377-417
+//   recombine_fragments proj/include/voxin/layers.hpp:477-520
+//
+// Bit-exactness: a window max is taken in the reference's scan order
+// (qx, qy, qz lexicographic) with the reference's update rule
+// `if (v > m) m = v` starting from the first element, so ties between +0 and
+// -0 resolve to the same element.  NaN inputs set the context flag, which the
+// host turns into VXG_INVALID like check_no_nan (layers.hpp:111-116).
+#include "common.cuh"
+
+namespace vxg {
+namespace {
+
+struct PoolGeom {
+  int64_t nx, ny, nz;     // input extents
+  int64_t mx, my, mz;     // output (fragment) extents
+  int px, py, pz;         // window
+  int P;                  // fragments per input entry (1 for plain pooling)
+  int64_t f;              // feature maps
+  int64_t b0;             // first output batch entry produced
+  int64_t nb;             // output batch entries produced
+};
+
+// One thread per output voxel, z fastest.  Output batch index b = s*P + off
+// with off = ox*py*pz + oy*pz + oz (layers.hpp:440-443); fragments with
+// P == 1 reduce to plain block pooling at offset 0.
+template <int PX, int PY, int PZ>
+__global__ void __launch_bounds__(256) pool_kernel(const float* __restrict__ in,
+                                                   float* __restrict__ out, PoolGeom g,
+                                                   int* __restrict__ nan_flag) {
+  const int px = PX > 0 ? PX : g.px, py = PY > 0 ? PY : g.py, pz = PZ > 0 ? PZ : g.pz;
+  const int64_t oel = g.mx * g.my * g.mz;
+  const int64_t total = g.nb * g.f * oel;
+  const int64_t nel = g.nx * g.ny * g.nz;
+  bool saw_nan = false;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = t % oel;
+    const int64_t bf = t / oel;
+    const int64_t fm = bf % g.f;
+    const int64_t b = g.b0 + bf / g.f;
+    const int64_t s = b / g.P;
+    const int off = static_cast<int>(b % g.P);
+    const int ox = g.P > 1 ? off / (py * pz) : 0;
+    const int oy = g.P > 1 ? (off / pz) % py : 0;
+    const int oz = g.P > 1 ? off % pz : 0;
+    const int64_t z = v % g.mz, y = (v / g.mz) % g.my, x = v / (g.mz * g.my);
+    const float* src = in + (s * g.f + fm) * nel;
+    const int64_t x0 = ox + x * px, y0 = oy + y * py, z0 = oz + z * pz;
+    float m = __ldg(src + (x0 * g.ny + y0) * g.nz + z0);
+    // px/py/pz are compile-time constants in the specialised instantiations
+#pragma unroll
+    for (int qx = 0; qx < px; ++qx)
+#pragma unroll
+      for (int qy = 0; qy < py; ++qy) {
+        const float* row = src + ((x0 + qx) * g.ny + y0 + qy) * g.nz + z0;
+#pragma unroll
+        for (int qz = 0; qz < pz; ++qz) {
+          const float val = __ldg(row + qz);
+          saw_nan |= (val != val);
+          m = val > m ? val : m;
+        }
+      }
+    out[t] = m;
+  }
+  if (saw_nan) *nan_flag = 1;
+}
+
+template <int PX, int PY, int PZ>
+void run_pool(Ctx* c, const float* in, float* out, const PoolGeom& g) {
+  const int64_t total = g.nb * g.f * g.mx * g.my * g.mz;
+  if (total == 0) return;
+  const unsigned grid = grid_for(total, 256, int64_t(c->num_sms) * 32);
+  pool_kernel<PX, PY, PZ><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
+  c->counted();
+  check_launch("pool_kernel");
+}
+
+void dispatch_pool(Ctx* c, const float* in, float* out, const PoolGeom& g) {
+  if (g.px == 2 && g.py == 2 && g.pz == 2)
+    run_pool<2, 2, 2>(c, in, out, g);
+  else if (g.px == 1 && g.py == 1 && g.pz == 1)
+    run_pool<1, 1, 1>(c, in, out, g);
+  else
+    run_pool<0, 0, 0>(c, in, out, g);
+}
+
+__global__ void nan_check_kernel(const float* __restrict__ x, int64_t n, int* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float v = __ldg(x + i);
+    bad |= (v != v);
+  }
+  if (bad) *flag = 1;
+}
+
+// Recombination as a gather: one thread per dense voxel (coalesced writes).
+// Dense coordinate d = off + x * stride per axis; off's mixed-radix digits
+// (cumulative stride before each window, layers.hpp:500-507) give the
+// per-window offsets, whose lexicographic indices form the fragment number
+// with the FIRST window slowest (layers.hpp:494-504).
+struct RecGeom {
+  int64_t nx, ny, nz;        // fragment extents
+  int64_t dx, dy, dz;        // dense extents
+  int64_t sx, sy, sz;        // total stride per axis
+  int64_t f, alpha, S0;
+  int nwin;
+  int win[8][3];
+  int64_t pre[8][3];         // cumulative stride before window w
+  int64_t scale[8];          // fragments per unit of window w's index
+};
+
+__global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict__ frag,
+                                                        float* __restrict__ dense, RecGeom g) {
+  const int64_t del = g.dx * g.dy * g.dz;
+  const int64_t total = g.S0 * g.f * del;
+  const int64_t nel = g.nx * g.ny * g.nz;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = t % del;
+    const int64_t sf = t / del;
+    const int64_t fm = sf % g.f, s = sf / g.f;
+    const int64_t dz = v % g.dz, dy = (v / g.dz) % g.dy, dx = v / (g.dz * g.dy);
+    const int64_t offx = dx % g.sx, offy = dy % g.sy, offz = dz % g.sz;
+    int64_t b = s * g.alpha;
+    for (int w = 0; w < g.nwin; ++w) {
+      const int64_t ox = (offx / g.pre[w][0]) % g.win[w][0];
+      const int64_t oy = (offy / g.pre[w][1]) % g.win[w][1];
+      const int64_t oz = (offz / g.pre[w][2]) % g.win[w][2];
+      b += ((ox * g.win[w][1] + oy) * g.win[w][2] + oz) * g.scale[w];
+    }
+    const int64_t x = dx / g.sx, y = dy / g.sy, z = dz / g.sz;
+    dense[t] = __ldg(frag + (b * g.f + fm) * nel + (x * g.ny + y) * g.nz + z);
+  }
+}
+
+}  // namespace
+
+void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 b0, i64 nb) {
+  PoolGeom g{n.x, n.y, n.z, n.x / p.x, n.y / p.y, n.z / p.z,
+             int(p.x), int(p.y), int(p.z), int(p.vol()), f, b0, nb};
+  (void)S;
+  dispatch_pool(c, in, out, g);
+}
+
+void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out) {
+  PoolGeom g{n.x, n.y, n.z, n.x / p.x, n.y / p.y, n.z / p.z, int(p.x), int(p.y), int(p.z), 1,
+             f, 0, S};
+  dispatch_pool(c, in, out, g);
+}
+
+void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
+                      const i64* windows, int nwin, float* dense, i64 S0) {
+  require(nwin <= 8, "recombine: at most 8 fragment windows supported");
+  require(b0 == 0, "recombine: partial fragment ranges are not supported");
+  RecGeom g{};
+  g.nx = n.x; g.ny = n.y; g.nz = n.z;
+  g.f = f; g.S0 = S0; g.nwin = nwin;
+  int64_t stride[3] = {1, 1, 1};
+  int64_t alpha = 1;
+  for (int w = 0; w < nwin; ++w) {
+    for (int a = 0; a < 3; ++a) {
+      g.win[w][a] = int(windows[3 * w + a]);
+      g.pre[w][a] = stride[a];
+      stride[a] *= windows[3 * w + a];
+    }
+    alpha *= windows[3 * w] * windows[3 * w + 1] * windows[3 * w + 2];
+  }
+  int64_t sc = alpha;
+  for (int w = 0; w < nwin; ++w) {
+    sc /= windows[3 * w] * windows[3 * w + 1] * windows[3 * w + 2];
+    g.scale[w] = sc;
+  }
+  g.alpha = alpha;
+  g.sx = stride[0]; g.sy = stride[1]; g.sz = stride[2];
+  g.dx = stride[0] * n.x; g.dy = stride[1] * n.y; g.dz = stride[2] * n.z;
+  require(nfrag == S0 * alpha, "recombine_fragments: fragment batch mismatch");
+  const int64_t total = S0 * f * g.dx * g.dy * g.dz;
+  if (total == 0) return;
+  recombine_kernel<<<grid_for(total, 256, int64_t(c->num_sms) * 32), 256, 0, c->stream>>>(
+      frag, dense, g);
+  c->counted();
+  check_launch("recombine_kernel");
+}
+
+void launch_nan_check(Ctx* c, const float* x, i64 count) {
+  if (count == 0) return;
+  nan_check_kernel<<<grid_for(count, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
+      x, count, c->d_flag);
+  c->counted();
+  check_launch("nan_check_kernel");
+}
+
+bool read_and_clear_flag(Ctx* c) {
+  int h = 0;
+  VXG_CUDA_CHECK(cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  VXG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return h != 0;
+}
+
+}  // namespace vxg

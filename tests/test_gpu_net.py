@@ -1,0 +1,102 @@
+"""GPU parity of the device-resident network forward (execute_plan with an
+all-fragment plan) against the reference run in fp64 on identical inputs and
+weights (oracle/make_golden.py), for toy nets and all four bundled nets at
+their smallest admissible extents; plus execution-shape invariants."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, rel_error
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north star: max-rel <= 1e-4 normalised by output magnitude
+
+
+def _run(v, ctx, text, m, algos):
+    net = v.parse_network_spec(text)
+    w = v.random_weights(net, m["wseed"])
+    x = v.fill_random(net.features_in * int(np.prod(m["extent"])), m["iseed"]).reshape(
+        (1, net.features_in) + tuple(m["extent"]))
+    out, rep = v.execute(net, w, x, ctx, conv_algos=algos)
+    return out, rep
+
+
+@pytest.mark.parametrize("algos", ["direct", "fft", None])
+def test_toy_nets(golden, ctx, algos):
+    import paper_1606_05688_b200 as v
+    meta = json.loads((GOLD / "nets.json").read_text())
+    g = golden("nets")
+    for name, m in meta.items():
+        out, rep = _run(v, ctx, m["text"], m, algos)
+        assert out.shape == tuple(m["out_shape"])
+        assert rel_error(out, g[f"{name}_out64"]) <= TOL, name
+        assert rep.voxels == np.prod(m["out_shape"][2:])
+
+
+@pytest.mark.parametrize("name", ["n337", "n726", "n926", "n537"])
+def test_bundled_nets(golden, ctx, name):
+    import paper_1606_05688_b200 as v
+    meta = json.loads((GOLD / "nets_bundled.json").read_text())
+    g = golden("nets_bundled")
+    m = meta[name]
+    out, rep = _run(v, ctx, m["text"], m, None)
+    assert out.shape == tuple(m["out_shape"])
+    err = rel_error(out, g[f"{name}_out64"])
+    assert err <= TOL, err
+    assert rep.seconds > 0 and len(rep.layer_seconds) == v.parse_network_spec(m["text"]).layer_count
+
+
+def test_forward_independent_of_budget_and_algorithm(ctx):
+    """Any feasible execution gives the same dense result (execute.hpp:384-386):
+    fragment groups forced small by the budget reproduce the unconstrained run
+    bit for bit (execute_test.cpp:188-227); FFT vs direct agree to tolerance."""
+    import torch
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    w = v.random_weights(net, 3)
+    x = torch.from_numpy(v.fill_random((1, 1, 100, 100, 100), 9)).cuda()
+    big, _ = v.Model(net, w, ctx).forward(x, conv_algos="fft")
+    need = v.Model(net, w, ctx).plan_bytes(1, 100, "fft")
+    assert need > 0
+    tight = v.Context(0, budget_bytes=int(need * 1.3) + (64 << 20))
+    small, _ = v.Model(net, w, tight).forward(x, conv_algos="fft")
+    assert torch.equal(big, small)
+    direct, _ = v.Model(net, w, ctx).forward(x, conv_algos="direct")
+    err = ((direct - big).abs().max() / direct.abs().max()).item()
+    assert err <= TOL
+    tight.close()
+
+
+def test_forward_translation_equivariance(ctx):
+    """Dense out[d] depends only on in[d, d+fov): a crop at an offset gives the
+    matching block of the full output (the large-config parity recipe)."""
+    import torch
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    w = v.random_weights(net, 1)
+    model = v.Model(net, w, ctx)
+    x = torch.from_numpy(v.fill_random((1, 1, 148, 148, 148), 1)).cuda()
+    full, _ = model.forward(x)
+    o = (24, 8, 40)
+    crop = x[:, :, o[0]:o[0] + 100, o[1]:o[1] + 100, o[2]:o[2] + 100].contiguous()
+    part, _ = model.forward(crop)
+    ref = full[:, :, o[0]:o[0] + 16, o[1]:o[1] + 16, o[2]:o[2] + 16]
+    err = ((part - ref).abs().max() / ref.abs().max()).item()
+    assert err <= TOL, err
+
+
+def test_forward_errors(ctx):
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    w = v.random_weights(net, 1)
+    with pytest.raises(ValueError, match="propagate"):
+        v.execute(net, w, np.zeros((1, 1, 93, 93, 93), np.float32), ctx)
+    tiny = v.Context(0, budget_bytes=64 << 20)
+    with pytest.raises(v.ResourceExhausted):
+        v.execute(net, w, np.zeros((1, 1, 148, 148, 148), np.float32), tiny)
+    tiny.close()

@@ -1,0 +1,209 @@
+"""GPU parity of every layer primitive and transform against the reference's
+golden vectors (oracle/make_golden.py) and the C oracle, through the C-ABI.
+
+Tolerances (north star: fp32, max-rel <= 1e-4 normalised by output magnitude):
+  * pools, MPF fragment order, recombination: bit-exact;
+  * convolutions: rel_error <= 1e-5 (direct) / 1e-4 (tiled FFT) vs fp64 reference;
+  * transforms: rel_error <= 1e-5 vs fp64 reference.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_error
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_pools_bit_exact(golden, ctx):
+    import paper_1606_05688_b200 as v
+    g = golden("pools")
+    out = v.max_pool(g["pin_pool_in"], (1, 1, 2), ctx).output
+    assert np.array_equal(out, g["pin_pool_out"])
+    out = v.mpf_pool(g["pin_mpf_in"], (1, 1, 2), ctx).output
+    assert out.reshape(-1).tolist() == [5, 3, 5, 9]
+    for i in range(int(g["ncases"])):
+        fn = v.mpf_pool if int(g[f"case{i}_kind"]) else v.max_pool
+        p = tuple(int(x) for x in g[f"case{i}_p"])
+        host = fn(g[f"case{i}_in"], p, ctx).output
+        assert np.array_equal(host, g[f"case{i}_out"]), i
+        dev = fn(_cuda(g[f"case{i}_in"]), p, ctx).output
+        assert np.array_equal(dev.cpu().numpy(), g[f"case{i}_out"]), i
+
+
+def test_mpf_random_vs_oracle_and_signed_zero(oracle, ctx):
+    import paper_1606_05688_b200 as v
+    rng = np.random.default_rng(5)
+    for shape, p in [((2, 3, 11, 9, 7), (2, 2, 2)), ((1, 2, 8, 11, 5), (3, 2, 3)),
+                     ((3, 1, 1, 1, 9), (1, 1, 5))]:
+        x = rng.standard_normal(shape).astype(np.float32)
+        x[x > 1.0] = 0.0
+        x[x < -1.0] = -0.0  # ties between +0 / -0 must resolve like the reference scan
+        got = v.mpf_pool(x, p, ctx).output
+        want = oracle.pool(True, x, p)
+        assert got.tobytes() == want.tobytes()
+
+
+def test_pool_errors(ctx):
+    import paper_1606_05688_b200 as v
+    with pytest.raises(ValueError, match="divisible"):
+        v.max_pool(np.zeros((1, 1, 5, 4, 4), np.float32), (2, 2, 2), ctx)
+    with pytest.raises(ValueError, match="extent\\+1"):
+        v.mpf_pool(np.zeros((1, 1, 4, 5, 5), np.float32), (2, 2, 2), ctx)
+    x = np.zeros((1, 1, 2, 2, 2), np.float32)
+    x.reshape(-1)[3] = np.nan
+    with pytest.raises(ValueError, match="NaN"):
+        v.max_pool(x, (1, 1, 1), ctx)
+    with pytest.raises(ValueError, match="NaN"):
+        v.mpf_pool(np.full((1, 1, 3, 3, 3), np.nan, np.float32), (2, 2, 2), ctx)
+    # window 1 is the identity (layers_test.cpp:106-108)
+    y = np.random.default_rng(1).standard_normal((2, 2, 3, 4, 5)).astype(np.float32)
+    assert np.array_equal(v.mpf_pool(y, (1, 1, 1), ctx).output, y)
+
+
+def test_recombine_bit_exact(golden, ctx):
+    import paper_1606_05688_b200 as v
+    g = golden("pools")
+    assert v.recombine_fragments(g["pin_rec_in"], [(1, 1, 2)], 1, ctx).reshape(-1).tolist() == [1, 3, 2, 4]
+    for i in range(int(g["nrec"])):
+        wins = [tuple(int(x) for x in w) for w in g[f"rec{i}_win"]]
+        got = v.recombine_fragments(g[f"rec{i}_in"], wins, int(g[f"rec{i}_S0"]), ctx)
+        assert np.array_equal(got, g[f"rec{i}_out"]), i
+        got = v.recombine_fragments(_cuda(g[f"rec{i}_in"]), wins, int(g[f"rec{i}_S0"]), ctx)
+        assert np.array_equal(got.cpu().numpy(), g[f"rec{i}_out"]), i
+    t = np.random.default_rng(3).standard_normal((3, 2, 2, 3, 4)).astype(np.float32)
+    assert np.array_equal(v.recombine_fragments(t, [], 3, ctx), t)
+    with pytest.raises(ValueError, match="mismatch"):
+        v.recombine_fragments(t, [(2, 2, 2)], 3, ctx)
+
+
+def test_mpf_then_recombine_is_dense_max_filter(ctx):
+    """layers_test.cpp:134-158: MPF + recombination == dense max filter, exactly."""
+    import paper_1606_05688_b200 as v
+    x = np.random.default_rng(34).standard_normal((2, 2, 9, 7, 11)).astype(np.float32)
+    p = (2, 2, 2)
+    frag = v.mpf_pool(x, p, ctx).output
+    dense = v.recombine_fragments(frag, [p], 2, ctx)
+    want = np.full((2, 2, 8, 6, 10), -np.inf, np.float32)
+    for qx in range(2):
+        for qy in range(2):
+            for qz in range(2):
+                want = np.maximum(want, x[:, :, qx:qx + 8, qy:qy + 6, qz:qz + 10])
+    assert np.array_equal(dense, want)
+
+
+@pytest.mark.parametrize("algo", ["direct", "fft"])
+def test_conv_matches_reference(golden, ctx, algo):
+    import paper_1606_05688_b200 as v
+    g = golden("conv")
+    tol = 1e-5 if algo == "direct" else 1e-4
+    fn = v.conv_direct if algo == "direct" else v.conv_fft_task_parallel
+    for i in range(int(g["ncases"])):
+        p = v.ConvLayerParams(g[f"c{i}_w"], g[f"c{i}_b"], "relu" if int(g[f"c{i}_relu"]) else "identity")
+        res = fn(g[f"c{i}_in"], p, ctx)
+        err = rel_error(res.output, g[f"c{i}_out64"])
+        assert err <= tol, (i, err)
+        assert res.audit.peak > 0
+
+
+def test_conv_device_pointers_and_fft_variants(golden, ctx):
+    import paper_1606_05688_b200 as v
+    g = golden("conv")
+    i = 6  # the 80 -> 80 k5 layer
+    p = v.ConvLayerParams(_cuda(g[f"c{i}_w"]), _cuda(g[f"c{i}_b"]), "relu")
+    for fn in (v.conv_fft_data_parallel, v.conv_fft_staged, v.conv_fft_task_parallel, v.conv_direct):
+        out = fn(_cuda(g[f"c{i}_in"]), p, ctx).output
+        assert rel_error(out.cpu().numpy(), g[f"c{i}_out64"]) <= 1e-4
+
+
+@pytest.mark.parametrize("case", [
+    (2, 8, (20, 18, 17), 8, (5, 3, 4)),
+    (1, 1, (40, 33, 35), 16, (4, 4, 4)),
+    (3, 4, (9, 9, 9), 5, (9, 9, 9)),
+    (1, 6, (30, 30, 30), 3, (7, 7, 7)),
+    (2, 5, (12, 13, 14), 7, (1, 1, 1)),
+])
+def test_conv_random_vs_oracle(oracle, ctx, case):
+    import paper_1606_05688_b200 as v
+    S, f, n, fo, k = case
+    rng = np.random.default_rng(sum(n) + fo)
+    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * np.prod(k)))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    want = oracle.conv(x, w, b, True)
+    p = v.ConvLayerParams(w, b, "relu")
+    assert rel_error(v.conv_direct(x, p, ctx).output, want) <= 1e-5
+    assert rel_error(v.conv_fft_staged(x, p, ctx).output, want) <= 1e-4
+
+
+def test_conv_fft_vs_direct_large(ctx):
+    """Size-independent property at a realistic layer size: FFT == direct."""
+    import torch
+    import paper_1606_05688_b200 as v
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.rand((2, 80, 70, 70, 70), device="cuda", generator=gen) * 2 - 1
+    w = (torch.rand((80, 80, 5, 5, 5), device="cuda", generator=gen) * 2 - 1) * (3.0 / (80 * 125)) ** 0.5
+    b = (torch.rand((80,), device="cuda", generator=gen) * 2 - 1) * 0.1
+    p = v.ConvLayerParams(w.contiguous(), b.contiguous(), "relu")
+    a = v.conv_direct(x, p, ctx).output
+    c = v.conv_fft_staged(x, p, ctx).output
+    err = (a - c).abs().max().item() / a.abs().max().item()
+    assert err <= 1e-4, err
+
+
+def test_conv_errors(ctx):
+    import paper_1606_05688_b200 as v
+    x = np.zeros((1, 2, 4, 4, 4), np.float32)
+    with pytest.raises(ValueError):
+        v.conv_direct(x, v.ConvLayerParams(np.zeros((1, 3, 2, 2, 2), np.float32), np.zeros(1, np.float32)), ctx)
+    with pytest.raises(ValueError):
+        v.conv_direct(x, v.ConvLayerParams(np.zeros((1, 2, 5, 2, 2), np.float32), np.zeros(1, np.float32)), ctx)
+    with pytest.raises(ValueError):
+        v.conv_direct(x, v.ConvLayerParams(np.zeros((2, 2, 2, 2, 2), np.float32), np.zeros(1, np.float32)), ctx)
+
+
+def test_conv_budget_exhausted():
+    import paper_1606_05688_b200 as v
+    small = v.Context(0, budget_bytes=1 << 20)
+    x = np.zeros((1, 8, 40, 40, 40), np.float32)  # 2 MB input alone
+    p = v.ConvLayerParams(np.zeros((8, 8, 3, 3, 3), np.float32), np.zeros(8, np.float32))
+    with pytest.raises(v.ResourceExhausted):
+        v.conv_fft_staged(x, p, small)
+    assert small.memory()["current"] == 0  # every charge unwound (layers_test.cpp:416-432)
+    small.close()
+
+
+def test_transforms_match_reference(golden, ctx):
+    import paper_1606_05688_b200 as v
+    g = golden("fft")
+    for i in range(int(g["ncases"])):
+        pad = tuple(int(x) for x in g[f"p{i}_pad"])
+        n = tuple(int(x) for x in g[f"p{i}_n"])
+        assert rel_error(v.pruned_fft_forward(g[f"p{i}_in"], pad, ctx), g[f"p{i}_nested"]) <= 1e-5
+        assert rel_error(v.pruned_fft_inverse(g[f"p{i}_nested"].astype(np.complex64), pad, n, ctx),
+                         g[f"p{i}_inv"]) <= 1e-5
+        assert rel_error(v.batched_fft_forward(g[f"p{i}_bin"], pad, ctx), g[f"p{i}_batched"]) <= 1e-5
+        assert rel_error(v.batched_fft_inverse(g[f"p{i}_batched"].astype(np.complex64), pad, n, ctx),
+                         g[f"p{i}_binv"]) <= 1e-5
+
+
+def test_transform_round_trip_large(ctx):
+    import paper_1606_05688_b200 as v
+    rng = np.random.default_rng(11)
+    for n, pad in [((161, 150, 97), (162, 150, 98)), ((78, 80, 66), (80, 80, 70))]:
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        s = v.pruned_fft_forward(x, pad, ctx)
+        assert rel_error(v.pruned_fft_inverse(s, pad, n, ctx), x) <= 1e-5
+        b = rng.uniform(-1, 1, (2,) + n).astype(np.float32)
+        sb = v.batched_fft_forward(b, pad, ctx)
+        assert rel_error(v.batched_fft_inverse(sb, pad, n, ctx), b) <= 1e-5
+        # nested and batched agree up to layout (fft_test.cpp:106-120)
+        s0 = v.pruned_fft_forward(b[0], pad, ctx)
+        zh = pad[2] // 2 + 1
+        full_b = np.transpose(sb[0], (2, 1, 0))  # (px, py, zh)
+        xh = pad[0] // 2 + 1
+        assert rel_error(full_b[:xh, :, :zh], s0[:, :, :zh]) <= 1e-5

@@ -1,0 +1,77 @@
+"""Kernel-level timing probe (not the driver's bench): times single layers on
+device-resident synthetic data with CUDA events on the library's stream.
+
+    python tools/kbench.py [--which conv,mpf,direct,net] [--n 256]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+import paper_1606_05688_b200 as v  # noqa: E402
+
+
+def timed(ctx, fn, reps=3):
+    s = torch.cuda.ExternalStream(ctx.stream())
+    fn()
+    ctx.sync()
+    times = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        b.synchronize()
+        times.append(a.elapsed_time(b) * 1e-3)
+    return min(times)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="conv,direct,mpf")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--T", type=int, default=0)
+    a = ap.parse_args()
+    ctx = v.Context(0)
+    res = {}
+    g = torch.Generator(device="cuda").manual_seed(1)
+    if "conv" in a.which:
+        n = a.n
+        x = torch.rand((1, 80, n, n, n), device="cuda", generator=g) * 2 - 1
+        w = (torch.rand((80, 80, 5, 5, 5), device="cuda", generator=g) * 2 - 1) * 0.02
+        b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
+        p = v.ConvLayerParams(w, b, "relu")
+        t = timed(ctx, lambda: v.conv_fft_staged(x, p, ctx))
+        no = n - 4
+        flops = 8.0 * 80 * 80 * (n ** 3) * 0  # placeholder
+        res["conv_fft_80x80_k5_n%d" % n] = {"s": t, "vox_per_s": no ** 3 / t}
+        del x
+    if "direct" in a.which:
+        n = 330
+        x = torch.rand((1, 1, n, n, n), device="cuda", generator=g) * 2 - 1
+        w = (torch.rand((80, 1, 4, 4, 4), device="cuda", generator=g) * 2 - 1) * 0.2
+        b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
+        p = v.ConvLayerParams(w, b, "relu")
+        t = timed(ctx, lambda: v.conv_direct(x, p, ctx))
+        no = n - 3
+        fl = 2.0 * 80 * 64 * no ** 3
+        res["direct_1x80_k4_n330"] = {"s": t, "tflops": fl / t / 1e12}
+    if "mpf" in a.which:
+        n = 255
+        x = torch.rand((1, 80, n, n, n), device="cuda", generator=g)
+        t = timed(ctx, lambda: v.mpf_pool(x, (2, 2, 2), ctx))
+        byt = 4.0 * 80 * (n ** 3 + 8 * 127 ** 3)
+        res["mpf_80x255"] = {"s": t, "GBps": byt / t / 1e9}
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
