@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""n537 sliding-window 3D ConvNet inference throughput on B200 (output voxels/s).
+
+One step = one device-resident forward of the bundled n537 network over one
+cubic input patch (synthetic: random_weights(net, 1) and the reference's
+fill_random generator), every pool as MPF, fragments recombined into the dense
+output.  The patch is the largest admissible extent (e = 2 mod 8) whose
+planned peak fits the HBM budget, unless --extent.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: one patch per GPU per step)
+
+Prints ONE JSON line (rank 0).  `value` is device-timed with inputs resident
+in HBM; `e2e` goes through the public API with pinned host buffers
+(H2D + forward + D2H inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NET = "n537"
+FFMA_FALLBACK_TFLOPS = 74.4  # 148 SM x 128 x 2 x 1.965 GHz (nominal), used only if measurement fails
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extent", type=int, default=0, help="cubic input extent (0: largest that fits)")
+    ap.add_argument("--budget-gb", type=float, default=0.0)
+    ap.add_argument("--cache-spectra", type=int, default=0,
+                    help="1: reuse kernel spectra across steps (weights fixed); 0: recompute per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--quick", action="store_true", help="small extent (profiling / smoke)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def bench_seed(seed, e):
+    """cli.cpp:261: the bench input seed for extent e."""
+    return (seed ^ ((0x9E3779B97F4A7C15 * e) & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pick_extent(model, budget_bytes, fov, hi=2048, stride=8, residue=2):
+    """Largest admissible extent (e = residue mod stride) whose plan fits."""
+    best = None
+    e = hi - ((hi - residue) % stride)
+    while e >= fov:
+        need = model.plan_bytes(1, e)
+        if 0 < need:
+            # device input + dense output of the timed run live outside the plan
+            extra = 4 * (e ** 3) + 4 * 3 * (e - fov + 1) ** 3
+            if need + extra <= budget_bytes:
+                best = e
+                break
+        e -= stride
+    return best
+
+
+def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm):
+    """sum over layers of max(F_l / P_fp32, B_l / P_hbm) with
+    F_fft = 7.5 S (f+f') N^3 log2 N + 2.5 f f' N log2 N (k^2 + kN + N^2) + 8 S f f' #w,
+    F_dir = 2 S f f' n'^3 k^3 (the cheaper conv per layer), MPF bytes
+    4 S f (n^3 + p^3 floor(n/p)^3); N = optimal_fft_size(n, device profile)."""
+    import math
+    from paper_1606_05688_b200 import optimal_fft_size
+    S, f, n = 1, 1, e
+    total = 0.0
+    for l in net_layers:
+        if l[0] == "conv":
+            fo, k = l[1], l[2][0]
+            no = n - k + 1
+            N = optimal_fft_size(n, "device")
+            lg = math.log2(N)
+            nw = N * N * (N // 2 + 1)
+            F_fft = 7.5 * S * (f + fo) * N ** 3 * lg + 2.5 * f * fo * N * lg * (k * k + k * N + N * N) \
+                + 8.0 * S * f * fo * nw
+            F_dir = 2.0 * S * f * fo * no ** 3 * k ** 3
+            B = 4.0 * (S * f * n ** 3 + S * fo * no ** 3 + f * fo * k ** 3 + fo)
+            total += max(min(F_fft, F_dir) / (peak_fp32 * 1e12), B / (peak_hbm * 1e9))
+            f, n = fo, no
+        else:
+            p = l[1][0]
+            m = n // p
+            B = 4.0 * S * f * (n ** 3 + p ** 3 * m ** 3)
+            total += B / (peak_hbm * 1e9)
+            S *= p ** 3
+            n = m
+    return total
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from the unmodified sources) on all host cores."""
+    if ws > 1 and rank != 0:
+        return
+    from oracle.refbind import Ref
+    from paper_1606_05688_b200.bundled_nets import FOV, NETS
+    ref = Ref(workers=0)
+    e = 170  # smallest admissible n537 patch: the largest one the CPU path finishes in bounded time
+    times = []
+    for i in range(args.warmup + args.steps):
+        secs, spent, vox = ref.net_sample(NETS[NET], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
+        if i >= args.warmup:
+            times.append(secs)
+    t = sum(times)
+    vox = (e - FOV[NET] + 1) ** 3
+    value = vox * len(times) / t
+    line = {
+        "impl": "reference", "metric": f"output voxels/sec, {NET} sliding-window inference",
+        "value": value, "unit": "voxels/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{NET} full forward, input {e}^3 -> dense 3x{e - FOV[NET] + 1}^3, "
+                               "all pools MPF, reference host primitives (direct for f=1 layers, "
+                               "fft_task_parallel otherwise)", "net": NET, "extent": e},
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
+                         "sample": f"full {NET} forward at the smallest admissible patch {e}^3 per step"},
+        "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline():
+    """Reference CPU path on the box's host cores (rank 0, N = 1): one full n537
+    forward at its smallest admissible patch through oracle/_ref."""
+    try:
+        from oracle.refbind import Ref
+        from paper_1606_05688_b200.bundled_nets import FOV, NETS
+    except Exception as ex:  # pragma: no cover
+        return {"value": None, "unit": "voxels/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {ex}"}
+    try:
+        ref = Ref(workers=0)
+    except FileNotFoundError as ex:
+        return {"value": None, "unit": "voxels/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {ex}"}
+    e = 170
+    secs, spent, vox = ref.net_sample(NETS[NET], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
+    return {"value": vox / secs, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
+            "seconds": secs,
+            "sample": f"one full {NET} forward at its smallest admissible patch {e}^3 -> dense "
+                      f"{e - FOV[NET] + 1}^3 (oracle/_ref built from the unmodified reference; "
+                      "direct conv for f=1 layers, fft_task_parallel otherwise; fp32)"}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import FOV, NETS
+
+    net = v.parse_network_spec(NETS[NET])
+    fov = FOV[NET]
+    weights = v.random_weights(net, 1)
+    peaks, peaks_src = measured_peaks()
+
+    budget = int(args.budget_gb * 1e9) if args.budget_gb > 0 else 0
+    ctx = v.Context(local, budget)
+    model = v.Model(net, weights, ctx)
+    budget_bytes = ctx.memory()["budget"]
+    if args.extent:
+        e = args.extent
+    elif args.quick:
+        e = 258
+    else:
+        e = pick_extent(model, budget_bytes * 0.97, fov)
+    if e is None:
+        raise SystemExit("no admissible extent fits the HBM budget")
+    dense = e - fov + 1
+    voxels = dense ** 3
+
+    # synthetic input (the reference's generator; rank-specific seed = another tile)
+    x_host = v.fill_random((1, 1, e, e, e), bench_seed(1 + rank, e))
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    x_dev = x_pin.cuda()
+    out_dev = torch.empty((1, 3, dense, dense, dense), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    cache = bool(args.cache_spectra)
+
+    def step():
+        model.forward(x_dev, out=out_dev, cache_spectra=cache)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+
+    ffma_peak = ctx.bench_ffma()
+    if not (ffma_peak > 1.0):
+        ffma_peak = FFMA_FALLBACK_TFLOPS
+
+    # ---- timed region (device events on the library stream) ----
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.sync()
+    clocks.start()
+    ctx.profile(True)
+    launches0 = ctx.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    ctx.sync()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    launches = ctx.launches - launches0
+    kstats = ctx.kernel_stats()
+    ctx.profile(False)
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    if ws > 1:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    value = ws * args.steps * voxels / elapsed
+
+    # ---- e2e through the public API, host buffers ----
+    out_host = torch.empty((1, 3, dense, dense, dense), dtype=torch.float32).pin_memory()
+    xin = x_pin.numpy()
+    oh = out_host.numpy()
+    model.forward(xin, out=oh, cache_spectra=cache)  # warm
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        model.forward(xin, out=oh, cache_spectra=cache)
+    e2e_t = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e = {"value": ws * args.e2e_steps * voxels / e2e_t, "unit": "voxels/s",
+           "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(oh.nbytes),
+           "steps": args.e2e_steps, "api": "vxg_model_forward(mem=HOST) via paper_1606_05688_b200.Model"}
+
+    # ---- roofline of the dominant kernel (live CUDA-event times) ----
+    kernels = {}
+    total_k = sum(s["seconds"] for s in kstats.values()) or 1.0
+    for name, s in kstats.items():
+        d = {"launches": s["launches"], "seconds": s["seconds"], "share": s["seconds"] / elapsed}
+        if s["flops"] > 0:
+            d["tflops"] = s["flops"] / s["seconds"] / 1e12
+        if s["bytes"] > 0:
+            d["gbps"] = s["bytes"] / s["seconds"] / 1e9
+        kernels[name] = d
+    dom = max(kstats, key=lambda k: kstats[k]["seconds"])
+    ds = kstats[dom]
+    if ds["flops"] > 0:
+        ach = ds["flops"] / ds["seconds"] / 1e12
+        roof = {"kernel": dom, "bound": "fp32", "achieved": ach, "peak": ffma_peak,
+                "unit": "TFLOP/s", "frac": ach / ffma_peak,
+                "peak_source": "measured FFMA microbenchmark (vxg_bench_ffma; MEASURED_PEAKS.json "
+                               "has no fp32 figure)"}
+    else:
+        ach = ds["bytes"] / ds["seconds"] / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src}
+    roof["traffic"] = None
+    roof["per_launch"] = {"flops": ds["flops"] / ds["launches"], "bytes": ds["bytes"] / ds["launches"],
+                          "seconds": ds["seconds"] / ds["launches"]}
+    t_roof = layer_roofline(net.layers, e, fov, ffma_peak, peaks["hbm_gbs"])
+    step_s = elapsed / args.steps
+    net_roof = {"seconds": t_roof, "step_seconds": step_s, "frac": t_roof / step_s,
+                "definition": "SURVEY 8(d): sum_l max(F_l/P_fp32, B_l/P_hbm), F = cheaper of "
+                              "whole-image pruned FFT and direct, P_fp32 = measured FFMA peak"}
+
+    line = {
+        "metric": f"output voxels/sec, {NET} 3D ConvNet sliding-window inference",
+        "value": value, "unit": "voxels/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{NET} full forward per GPU, input patch {e}^3 -> dense 3x{dense}^3 "
+                               "(largest admissible patch fitting the HBM budget)",
+                   "net": NET, "extent": e, "dense_out": dense, "global_batch": ws,
+                   "parallelism": f"independent halo patches x{ws}",
+                   "kernel_spectra": "cached across steps" if cache else "recomputed every step",
+                   "l2": "inputs and activations >> 126 MB L2 (no flush needed)"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "roofline": roof,
+        "layer_roofline": net_roof,
+        "kernels": kernels,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    model.close()
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

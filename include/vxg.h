@@ -83,6 +83,30 @@ int vxg_ctx_reset_peak(vxg_ctx* ctx);
 /* number of kernels this context launched so far (for launch accounting) */
 int64_t vxg_ctx_launches(vxg_ctx* ctx);
 
+/* Kernel families for per-launch instrumentation. */
+enum vxg_kernel_kind {
+  VXG_K_TILE_FWD = 0, /* K1: forward tile transform (images) */
+  VXG_K_TILE_INV = 1, /* K4: inverse tile transform + crop/bias/ReLU */
+  VXG_K_CGEMM = 2,    /* K3: per-frequency complex contraction */
+  VXG_K_KSPEC = 3,    /* K2: kernel spectra */
+  VXG_K_DIRECT = 4,   /* K5: direct convolution */
+  VXG_K_POOL = 5,     /* K6: MPF / max pooling */
+  VXG_K_RECOMBINE = 6,/* K7: fragment recombination */
+  VXG_K_LINEFFT = 7,  /* whole-image transform lines */
+  VXG_K_OTHER = 8,
+  VXG_K_COUNT = 9
+};
+/* enable != 0: start recording CUDA events around every launch (clears old
+ * records); 0: stop. */
+int vxg_ctx_profile(vxg_ctx* ctx, int enable);
+/* Aggregate of the recorded launches of one kind: count, summed device
+ * seconds, summed algorithmic flops and bytes (synchronises the stream). */
+int vxg_ctx_kernel_stats(vxg_ctx* ctx, int kind, int64_t* launches, double* seconds,
+                         double* flops, double* bytes);
+/* FFMA throughput microbenchmark (TFLOP/s, fp32, all SMs): the roofline
+ * denominator of the FFMA kernels (MEASURED_PEAKS.json has no fp32 figure). */
+int vxg_bench_ffma(vxg_ctx* ctx, double* tflops);
+
 /* ---- layer primitives (include/voxin/layers.hpp) -------------------------- */
 
 /* conv_direct / conv_fft_* (layers.hpp:142-371, task_conv.hpp:415-442):

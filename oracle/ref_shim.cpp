@@ -402,12 +402,17 @@ int ref_net_sample(const char* net_text, int64_t e, uint64_t wseed, uint64_t ise
     for (const auto& l : net.layers) {
       const auto t0 = clk::now();
       if (std::holds_alternative<ConvSpec>(l)) {
-        x = run_conv<float>(conv_kind, std::move(x), w.convs[ci++]);
+        // conv_kind < 0: the reference's fastest measured host primitive per
+        // layer -- direct for single-input-map layers, task-parallel FFT else
+        const int kind = conv_kind >= 0 ? conv_kind : (x.shape().f == 1 ? 0 : 3);
+        x = run_conv<float>(kind, std::move(x), w.convs[ci++]);
       } else {
         const vec3 p = std::get<PoolSpec>(l).window;
         x = mpf_pool(std::move(x), p, ctx).output;
         const i64 have = x.shape().s;
-        const i64 k = keep > 0 ? std::min<i64>(keep, have) : have;
+        // sample only at the FIRST pool: later layers keep running batched,
+        // so per-call overheads are charged as in the full run
+        const i64 k = (keep > 0 && mult == 1.0) ? std::min<i64>(keep, have) : have;
         const double dt0 = std::chrono::duration<double>(clk::now() - t0).count();
         total += dt0 * mult;
         spent += dt0;

@@ -73,6 +73,10 @@ def lib() -> C.CDLL:
         "vxg_ctx_memory": (I, [P, A, A, A]),
         "vxg_ctx_reset_peak": (I, [P]),
         "vxg_ctx_launches": (I64, [P]),
+        "vxg_ctx_profile": (I, [P, I]),
+        "vxg_ctx_kernel_stats": (I, [P, I, A, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)]),
+        "vxg_bench_ffma": (I, [P, C.POINTER(C.c_double)]),
         "vxg_conv": (I, [P, I, I, P, I64, I64, A, P, I64, A, P, I, P, C.POINTER(Audit)]),
         "vxg_max_pool": (I, [P, I, P, I64, I64, A, A, P, C.POINTER(Audit)]),
         "vxg_mpf_pool": (I, [P, I, P, I64, I64, A, A, P, C.POINTER(Audit)]),

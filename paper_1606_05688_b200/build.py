@@ -2,7 +2,9 @@
 (-gencode arch=compute_100a,code=sm_100a -lineinfo), linked into one shared
 library with the static CUDA runtime.  Also used by __graft_entry__.build().
 
-    python -m paper_1606_05688_b200.build [--verbose-ptxas]
+    python paper_1606_05688_b200/build.py [--verbose-ptxas]
+
+(run by path: importing the package itself needs the built library)
 """
 from __future__ import annotations
 

@@ -205,6 +205,51 @@ int vxg_ctx_reset_peak(vxg_ctx* ctx) {
 
 int64_t vxg_ctx_launches(vxg_ctx* ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->launches.load() : -1; }
 
+int vxg_ctx_profile(vxg_ctx* ctx, int enable) {
+  return guard([&] {
+    Ctx* c = ctx_of(ctx);
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    if (enable) {
+      for (auto& r : c->krec) {
+        c->spare_events.push_back(r.a);
+        c->spare_events.push_back(r.b);
+      }
+      c->krec.clear();
+    }
+    c->prof = enable != 0;
+  });
+}
+
+int vxg_ctx_kernel_stats(vxg_ctx* ctx, int kind, int64_t* launches, double* seconds,
+                         double* flops, double* bytes) {
+  return guard([&] {
+    Ctx* c = ctx_of(ctx);
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    int64_t n = 0;
+    double s = 0, fl = 0, by = 0;
+    for (const auto& r : c->krec) {
+      if (r.kind != kind) continue;
+      float ms = 0;
+      VXG_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+      ++n;
+      s += ms * 1e-3;
+      fl += r.flops;
+      by += r.bytes;
+    }
+    if (launches) *launches = n;
+    if (seconds) *seconds = s;
+    if (flops) *flops = fl;
+    if (bytes) *bytes = by;
+  });
+}
+
+int vxg_bench_ffma(vxg_ctx* ctx, double* tflops) {
+  return guard([&] {
+    need(tflops, "vxg_bench_ffma");
+    *tflops = bench_ffma(ctx_of(ctx));
+  });
+}
+
 // ---- layer primitives ---------------------------------------------------------
 
 int vxg_conv(vxg_ctx* ctx, int algo, int mem, const float* in, int64_t S, int64_t f,

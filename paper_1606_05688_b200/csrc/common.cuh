@@ -11,6 +11,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "vxg.h"
 
@@ -53,6 +54,14 @@ struct V3 {
   static V3 cube(i64 e) { return V3{e, e, e}; }
 };
 
+// Per-launch instrumentation record (CUDA events on the launching stream plus
+// the launch's ALGORITHMIC flops / bytes), enabled by vxg_ctx_profile().
+struct KRecord {
+  int kind;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
 // One context per GPU.  All work is issued on `stream`; allocations are
 // stream-ordered (cudaMallocAsync) and charged against `budget` bytes.
 struct Ctx {
@@ -66,6 +75,20 @@ struct Ctx {
   int* d_flag = nullptr;  // device error flag (NaN seen by pools)
   std::atomic<i64> launches{0};
   std::mutex mu;
+  bool prof = false;
+  std::vector<KRecord> krec;
+  std::vector<cudaEvent_t> spare_events;
+
+  cudaEvent_t take_event() {
+    if (!spare_events.empty()) {
+      cudaEvent_t e = spare_events.back();
+      spare_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) throw cuda_failure("cudaEventCreate failed");
+    return e;
+  }
 
   void charge(i64 bytes) {
     std::lock_guard<std::mutex> lk(mu);
@@ -80,6 +103,27 @@ struct Ctx {
     current -= bytes;
   }
   void counted(i64 n = 1) { launches += n; }
+};
+
+// Brackets one kernel launch with events when profiling is on.
+class KScope {
+ public:
+  KScope(Ctx* c, int kind, double flops, double bytes) : c_(c) {
+    if (!c_->prof) return;
+    rec_ = KRecord{kind, c_->take_event(), c_->take_event(), flops, bytes};
+    cudaEventRecord(rec_.a, c_->stream);
+  }
+  ~KScope() {
+    if (!c_->prof) return;
+    cudaEventRecord(rec_.b, c_->stream);
+    c_->krec.push_back(rec_);
+  }
+  KScope(const KScope&) = delete;
+  KScope& operator=(const KScope&) = delete;
+
+ private:
+  Ctx* c_;
+  KRecord rec_{};
 };
 
 // RAII device buffer charged against the context budget.
@@ -153,6 +197,9 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
                       const i64* windows, int nwin, float* dense, i64 S0);
 void launch_nan_check(Ctx* c, const float* x, i64 count);
 bool read_and_clear_flag(Ctx* c);
+
+// instrumentation (k_misc.cu)
+double bench_ffma(Ctx* c);
 
 // direct convolution (k_direct.cu)
 void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float* w, i64 fo,

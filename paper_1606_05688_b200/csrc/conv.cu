@@ -59,6 +59,7 @@ void compute_kernel_spectra(Ctx* c, int T, const float* w, int64_t fo, int64_t f
   a.mstride = fo;
   a.out = out;
   a.scale = float(1.0 / (double(T) * double(T) * double(T)));
+  a.kind = VXG_K_KSPEC;
   launch_tile_fwd(c, T, a, fo * f);
 }
 
@@ -110,6 +111,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ga.mstride = rows;
     ga.f = int(f);
     ga.fo = int(fo);
+    ga.T = T;
     launch_cgemm(c, ga, plan.nwb);
 
     InvTileArgs ia{};

@@ -20,6 +20,7 @@ struct FwdTileArgs {
   int64_t mstride;           // rows of the spectrum buffer (layout stride)
   float2* out;               // [w/16][mstride][f][16]
   float scale;
+  int kind = VXG_K_TILE_FWD; // instrumentation family (images or kernel spectra)
 };
 
 struct InvTileArgs {
@@ -46,6 +47,7 @@ struct GemmArgs {
   int64_t mstride;
   int f, fo;
   int mblocks, iblocks;
+  int T;                     // tile size (for the algorithmic flop count)
 };
 
 extern const int kTileSizes[];

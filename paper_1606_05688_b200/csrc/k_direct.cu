@@ -157,6 +157,10 @@ void run_direct(Ctx* c, const float* in, const float* w, const float* bias, floa
   }
   dim3 grid(unsigned(g.tiles_x) * g.tiles_y * g.tiles_z, unsigned((g.fo + JB - 1) / JB),
             unsigned(g.S));
+  const double vox = double(g.ox) * g.oy * g.oz;
+  KScope ks(c, VXG_K_DIRECT, 2.0 * double(g.S) * g.f * g.fo * vox * double(kvol),
+            4.0 * (double(g.S) * g.f * g.nx * g.ny * g.nz + double(g.S) * g.fo * vox +
+                   double(g.fo) * g.f * kvol));
   conv_direct_kernel<KZ><<<grid, THREADS, smem, c->stream>>>(in, w, bias, out, g);
   c->counted();
   check_launch("conv_direct_kernel");

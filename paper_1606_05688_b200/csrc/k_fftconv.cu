@@ -441,6 +441,8 @@ const int kNumTileSizes = sizeof(kTileSizes) / sizeof(int);
 int64_t tile_nwb(int T) { return (int64_t(T) * T * (T / 2 + 1) + WB - 1) / WB; }
 
 void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks) {
+  const double nw = double(T) * T * (T / 2 + 1);
+  KScope ks(c, a.kind, 0.0, double(nblocks) * (4.0 * double(T) * T * T + 8.0 * nw));
   switch (T) {
     case 4: fwd_t<4>(c, a, nblocks); break;
     case 6: fwd_t<6>(c, a, nblocks); break;
@@ -458,6 +460,9 @@ void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks) {
 }
 
 void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a, int64_t nblocks) {
+  const double nw = double(T) * T * (T / 2 + 1);
+  KScope ks(c, VXG_K_TILE_INV, 0.0,
+            double(nblocks) * (8.0 * nw + 4.0 * double(a.vx) * a.vy * a.vz));
   switch (T) {
     case 4: inv_t<4>(c, a, nblocks); break;
     case 6: inv_t<6>(c, a, nblocks); break;
@@ -475,6 +480,9 @@ void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a, int64_t nblocks) {
 }
 
 void launch_cgemm(Ctx* c, const GemmArgs& a, int64_t nwb) {
+  const double nw = double(a.T) * a.T * (a.T / 2 + 1);  // true (unpadded) frequencies
+  KScope ks(c, VXG_K_CGEMM, 8.0 * double(a.M) * a.f * a.fo * nw,
+            8.0 * nw * (double(a.M) * a.f + double(a.M) * a.fo + double(a.f) * a.fo));
   if (a.fo >= 24)
     gemm_t<8, 5, 32, 40, 8>(c, a, nwb);
   else

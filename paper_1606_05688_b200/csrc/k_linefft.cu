@@ -146,6 +146,7 @@ void run_lines(Ctx* c, LineJob j, int64_t n0) {
   j.nlines = n0 * j.nl1 * j.nl2;
   if (j.nlines == 0) return;
   require(j.nlines < (int64_t(1) << 31), "device line transform: too many lines");
+  KScope ks(c, VXG_K_LINEFFT, 0.0, 16.0 * double(j.nlines) * j.N);
   line_fft_kernel<<<unsigned(j.nlines), kLineThreads, 0, c->stream>>>(j);
   c->counted();
   check_launch("line_fft_kernel");

@@ -76,6 +76,7 @@ void run_pool(Ctx* c, const float* in, float* out, const PoolGeom& g) {
   const int64_t total = g.nb * g.f * g.mx * g.my * g.mz;
   if (total == 0) return;
   const unsigned grid = grid_for(total, 256, int64_t(c->num_sms) * 32);
+  KScope ks(c, VXG_K_POOL, 0.0, 8.0 * double(total));  // read ~= write (P m^3 ~= n^3)
   pool_kernel<PX, PY, PZ><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
   c->counted();
   check_launch("pool_kernel");
@@ -183,6 +184,7 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
   require(nfrag == S0 * alpha, "recombine_fragments: fragment batch mismatch");
   const int64_t total = S0 * f * g.dx * g.dy * g.dz;
   if (total == 0) return;
+  KScope ks(c, VXG_K_RECOMBINE, 0.0, 8.0 * double(total));
   recombine_kernel<<<grid_for(total, 256, int64_t(c->num_sms) * 32), 256, 0, c->stream>>>(
       frag, dense, g);
   c->counted();
@@ -191,6 +193,7 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
 
 void launch_nan_check(Ctx* c, const float* x, i64 count) {
   if (count == 0) return;
+  KScope ks(c, VXG_K_OTHER, 0.0, 4.0 * double(count));
   nan_check_kernel<<<grid_for(count, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
       x, count, c->d_flag);
   c->counted();

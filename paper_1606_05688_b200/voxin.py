@@ -87,6 +87,31 @@ class Context:
     def launches(self) -> int:
         return int(lib().vxg_ctx_launches(self._p))
 
+    KERNEL_KINDS = ("tile_fwd", "tile_inv", "cgemm", "kspec", "direct", "pool", "recombine",
+                    "linefft", "other")
+
+    def profile(self, enable: bool):
+        """Record CUDA events around every launch (per-kernel device time)."""
+        check(lib().vxg_ctx_profile(self._p, 1 if enable else 0))
+
+    def kernel_stats(self):
+        """{kind: {launches, seconds, flops, bytes}} of the recorded launches."""
+        out = {}
+        for i, name in enumerate(self.KERNEL_KINDS):
+            n = C.c_int64()
+            s, fl, by = C.c_double(), C.c_double(), C.c_double()
+            check(lib().vxg_ctx_kernel_stats(self._p, i, C.byref(n), C.byref(s), C.byref(fl),
+                                             C.byref(by)))
+            if n.value:
+                out[name] = {"launches": n.value, "seconds": s.value, "flops": fl.value,
+                             "bytes": by.value}
+        return out
+
+    def bench_ffma(self) -> float:
+        t = C.c_double()
+        check(lib().vxg_bench_ffma(self._p, C.byref(t)))
+        return t.value
+
     def close(self):
         if self._p:
             lib().vxg_ctx_destroy(self._p)
