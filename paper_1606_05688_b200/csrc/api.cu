@@ -338,7 +338,7 @@ static int pool_common(vxg_ctx* ctx, int fragments, int mem, const float* in, in
     if (read_and_clear_flag(c))
       throw invalid(std::string(fragments ? "mpf_pool" : "max_pool") + ": NaN input rejected");
     if (fragments)
-      launch_mpf(c, xin.p, S, f, n, p, o.p, 0, S * P);
+      launch_mpf(c, xin.p, S, f, n, p, o.p);
     else
       launch_maxpool(c, xin.p, S, f, n, p, o.p);
     o.finish(c);

@@ -191,7 +191,10 @@ inline void check_launch(const char* what) {
 // ---- kernel entry points (implemented in the k_*.cu units) -----------------
 
 // pools (k_pool.cu)
-void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 b0, i64 nb);
+// MPF of S whole entries (all P fragments); the output may be the channel
+// slice [c0, c0+f) of a tensor with f_tot channels (f_tot <= 0: f)
+void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot = 0,
+                i64 c0 = 0);
 void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out);
 void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
                       const i64* windows, int nwin, float* dense, i64 S0);

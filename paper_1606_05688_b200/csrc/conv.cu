@@ -4,6 +4,7 @@
 // reference's transform scratch (proj/include/voxin/fft.hpp:74-90).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "fftconv.hpp"
@@ -18,6 +19,13 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
   FftPlan best;
   best.cost = std::numeric_limits<double>::infinity();
   const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
+  if (T_forced <= 0) {
+    // experiment hook: VXG_FFT_TILE=<T> pins the tile size when it covers the kernel
+    if (const char* env = std::getenv("VXG_FFT_TILE")) {
+      const int t = std::atoi(env);
+      if (t >= k.x && t >= k.y && t >= k.z) T_forced = t;
+    }
+  }
   for (int ti = 0; ti < kNumTileSizes; ++ti) {
     const int T = kTileSizes[ti];
     if (T_forced > 0 && T != T_forced) continue;

@@ -104,57 +104,79 @@ ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos) const {
 
 namespace {
 
-// Peak-memory model of running layers [li, L) on B entries (input included),
-// with the executor's greedy group choice below each MPF.
-struct PeakModel {
+// One execution step starting at layer li: a single layer, or a direct conv
+// fused with the MPF that follows it (conv output produced and pooled one
+// channel block at a time, so the full-resolution conv output never exists).
+struct Step {
+  size_t li, next;
+  bool fused;
+  int64_t P;  // entries produced per input entry
+};
+
+// Memory model of the executor.  need_min[li] is the peak (bytes, input of
+// layer li excluded) of running layers [li, L) on ONE entry with groups of one
+// entry everywhere below -- independent of the batch, so the greedy group
+// choice at each level is a single binary search.
+struct Sched {
   const Model& m;
   const ForwardPlan& p;
   bool cache;
+  std::vector<int64_t> need_min;
 
-  int64_t conv_ws(size_t li, int64_t B) const {
-    const LayerChoice& ch = p.choice[li];
-    if (ch.algo != VXG_CONV_FFT) return 0;
-    const Shape& in = p.shapes[li];
-    const int64_t fo = m.net.layers[li].fo;
-    const int64_t M = B * ch.fft.tiles;
-    const int64_t rows = std::min<int64_t>(M, 256);
-    int64_t ws = fft_chunk_bytes(ch.fft, in.f, fo, rows);
-    if (!cache) ws += ch.fft.nwb * fo * in.f * 16 * 8;
-    return ws;
-  }
-
-  int64_t peak(size_t li, int64_t B, int64_t avail) const {
+  Sched(const Model& mm, const ForwardPlan& pp, bool c) : m(mm), p(pp), cache(c) {
     const size_t L = m.net.layers.size();
-    if (li >= L) return 0;
-    const int64_t in = B * entry_bytes(p.shapes[li]);
-    const Layer& l = m.net.layers[li];
-    const bool last = li + 1 == L;
-    if (l.kind == 0) {
-      const int64_t out = last ? 0 : B * entry_bytes(p.shapes[li + 1]);
-      const int64_t here = in + out + conv_ws(li, B);
-      const int64_t next = last ? 0 : peak(li + 1, B, avail);
-      return std::max(here, next);
+    need_min.assign(L + 1, 0);
+    for (size_t li = L; li-- > 0;) {
+      const Step st = step(li);
+      // the P entries this makes are processed one at a time below
+      need_min[li] = out_bytes(st, 1) + std::max(ws_bytes(st, 1), st.next < L ? need_min[st.next] : 0);
     }
-    if (last) return in;
-    if (p.pool_mode[li] == 0) {
-      const int64_t out = B * entry_bytes(p.shapes[li + 1]);
-      return std::max(in + out, peak(li + 1, B, avail));
-    }
-    const int64_t G = choose(li, B, avail);
-    return in + peak(li + 1, G, avail - in);
   }
 
-  // largest fragment group (output entries per pass) that fits `avail`
-  int64_t choose(size_t li, int64_t B, int64_t avail) const {
-    const int64_t total = B * m.net.layers[li].ext.vol();
-    const int64_t in = B * entry_bytes(p.shapes[li]);
-    const int64_t room = avail - in;
-    if (peak(li + 1, total, room) <= room) return total;
-    int64_t lo = 1, hi = total;
-    if (peak(li + 1, 1, room) > room) return 1;
+  Step step(size_t li) const {
+    const size_t L = m.net.layers.size();
+    const Layer& l = m.net.layers[li];
+    if (l.kind == 0 && p.choice[li].algo == VXG_CONV_DIRECT && li + 1 < L &&
+        m.net.layers[li + 1].kind == 1 && p.pool_mode[li + 1] == 1)
+      return Step{li, li + 2, true, m.net.layers[li + 1].ext.vol()};
+    const int64_t P = (l.kind == 1 && p.pool_mode[li] == 1) ? l.ext.vol() : 1;
+    return Step{li, li + 1, false, P};
+  }
+
+  int64_t out_bytes(const Step& st, int64_t g) const {
+    if (st.next >= m.net.layers.size()) return 0;  // leaves write the final buffer
+    return g * st.P * entry_bytes(p.shapes[st.next]);
+  }
+
+  // channel block of the fused direct conv: multiple of 16 maps
+  int64_t fused_block_bytes(const Step& st, int64_t g, int64_t cb) const {
+    const Shape& mid = p.shapes[st.li + 1];
+    return g * cb * mid.n.vol() * 4;
+  }
+
+  int64_t ws_bytes(const Step& st, int64_t g) const {
+    const Layer& l = m.net.layers[st.li];
+    if (st.fused) return fused_block_bytes(st, g, std::min<int64_t>(16, l.fo));
+    if (l.kind != 0 || p.choice[st.li].algo != VXG_CONV_FFT) return 0;
+    const LayerChoice& ch = p.choice[st.li];
+    const Shape& in = p.shapes[st.li];
+    const int64_t M = g * ch.fft.tiles;
+    return fft_chunk_bytes(ch.fft, in.f, l.fo, std::min<int64_t>(M, 256));
+  }
+
+  int64_t group_need(const Step& st, int64_t g) const {
+    const size_t L = m.net.layers.size();
+    const int64_t rec = st.next < L ? need_min[st.next] : 0;
+    return out_bytes(st, g) + std::max(ws_bytes(st, g), rec);
+  }
+
+  // largest group (entries of layer li's input) whose step fits `avail`
+  int64_t choose(const Step& st, int64_t B, int64_t avail) const {
+    if (group_need(st, B) <= avail) return B;
+    int64_t lo = 1, hi = B;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) / 2;
-      if (peak(li + 1, mid, room) <= room)
+      if (group_need(st, mid) <= avail)
         lo = mid;
       else
         hi = mid - 1;
@@ -202,105 +224,98 @@ struct Runner {
   Model& m;
   const ForwardPlan& p;
   bool cache;
+  Sched sched;
   float* final_frags;
   int64_t final_off = 0;
   EventTimer& timer;
 
-  float* final_slot() const {
-    return final_frags + final_off * entry_bytes(p.shapes.back()) / 4;
+  int64_t avail() const {
+    std::lock_guard<std::mutex> lk(m.c->mu);
+    return m.c->budget - m.c->current;
   }
 
-  void run(size_t li, const float* in, DevBuf* owner, int64_t B) {
+  // run layers [li, L) on B entries of layer li's input at `in` (not owned)
+  void run(size_t li, const float* in, int64_t B) {
     const size_t L = m.net.layers.size();
+    const Step st = sched.step(li);
+    const int64_t G = sched.choose(st, B, avail());
+    const int64_t in_entry = entry_bytes(p.shapes[li]) / 4;
+    for (int64_t b0 = 0; b0 < B; b0 += G) {
+      const int64_t g = std::min(G, B - b0);
+      const bool leaf = st.next >= L;
+      DevBuf out;
+      float* dst;
+      if (leaf) {
+        dst = final_frags + final_off * (entry_bytes(p.shapes.back()) / 4);
+      } else {
+        out.alloc(m.c, sched.out_bytes(st, g));
+        dst = out.as<float>();
+      }
+      exec(st, in + b0 * in_entry, g, dst);
+      if (leaf)
+        final_off += g * st.P;
+      else
+        run(st.next, dst, g * st.P);
+    }
+  }
+
+  void exec(const Step& st, const float* in, int64_t g, float* dst) {
+    const size_t li = st.li;
     const Layer& l = m.net.layers[li];
     const Shape& si = p.shapes[li];
-    const Shape& so = p.shapes[li + 1];
-    const bool last = li + 1 == L;
-    if (l.kind == 0) {
-      DevBuf out;
-      float* dst = last ? final_slot() : nullptr;
-      if (!last) {
-        out.alloc(m.c, B * entry_bytes(so));
-        dst = out.as<float>();
-      }
+    if (st.fused) {
+      // direct conv one channel block at a time, each block pooled straight
+      // into its channel slice of the MPF output
+      const Layer& pool = m.net.layers[li + 1];
+      const Shape& mid = p.shapes[li + 1];
       const int ci = m.conv_index[li];
-      const int h = timer.begin(li);
+      const int64_t per_ch = g * mid.n.vol() * 4;
+      int64_t cb = std::max<int64_t>(1, avail() / std::max<int64_t>(per_ch, 1));
+      cb = std::min(cb, l.fo);
+      if (cb >= 16) cb -= cb % 16;
+      DevBuf tmp(m.c, cb * per_ch);
+      const int64_t kvol = l.ext.vol();
+      for (int64_t c0 = 0; c0 < l.fo; c0 += cb) {
+        const int64_t n = std::min(cb, l.fo - c0);
+        int h = timer.begin(li);
+        conv_direct_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>() + c0 * si.f * kvol,
+                           n, l.ext, m.bias[size_t(ci)].as<float>() + c0, l.relu, tmp.as<float>());
+        timer.end(h);
+        h = timer.begin(li + 1);
+        launch_mpf(m.c, tmp.as<float>(), g, n, mid.n, pool.ext, dst, l.fo, c0);
+        timer.end(h);
+      }
+      return;
+    }
+    const int h = timer.begin(li);
+    if (l.kind == 0) {
+      const int ci = m.conv_index[li];
       if (p.choice[li].algo == VXG_CONV_FFT) {
         const float2* ws = m.spectra_for(ci, p.choice[li].fft.T, cache);
-        conv_fft_device(m.c, in, B, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
+        conv_fft_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
                         m.bias[size_t(ci)].as<float>(), l.relu, dst, p.choice[li].fft, ws, 0);
       } else {
-        conv_direct_device(m.c, in, B, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
+        conv_direct_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
                            m.bias[size_t(ci)].as<float>(), l.relu, dst);
       }
-      timer.end(h);
-      if (owner) owner->reset();
-      if (last) {
-        final_off += B;
-        return;
-      }
-      run(li + 1, dst, &out, B);
-      return;
+    } else if (p.pool_mode[li] == 1) {
+      launch_mpf(m.c, in, g, si.f, si.n, l.ext, dst);
+    } else {
+      launch_maxpool(m.c, in, g, si.f, si.n, l.ext, dst);
     }
-    // pooling
-    if (p.pool_mode[li] == 0) {
-      DevBuf out;
-      float* dst = last ? final_slot() : nullptr;
-      if (!last) {
-        out.alloc(m.c, B * entry_bytes(so));
-        dst = out.as<float>();
-      }
-      const int h = timer.begin(li);
-      launch_maxpool(m.c, in, B, si.f, si.n, l.ext, dst);
-      timer.end(h);
-      if (owner) owner->reset();
-      if (last) {
-        final_off += B;
-        return;
-      }
-      run(li + 1, dst, &out, B);
-      return;
-    }
-    const int64_t total = B * l.ext.vol();
-    int64_t G = total;
-    if (!last) {
-      PeakModel pm{m, p, cache};
-      int64_t avail;
-      {
-        std::lock_guard<std::mutex> lk(m.c->mu);
-        avail = m.c->budget - m.c->current;
-      }
-      G = pm.choose(li, B, avail + B * entry_bytes(si));
-    }
-    for (int64_t b0 = 0; b0 < total; b0 += G) {
-      const int64_t g = std::min(G, total - b0);
-      DevBuf out;
-      float* dst = last ? final_slot() : nullptr;
-      if (!last) {
-        out.alloc(m.c, g * entry_bytes(so));
-        dst = out.as<float>();
-      }
-      const int h = timer.begin(li);
-      launch_mpf(m.c, in, B, si.f, si.n, l.ext, dst, b0, g);
-      timer.end(h);
-      if (last) {
-        final_off += g;
-        continue;
-      }
-      run(li + 1, dst, &out, g);
-    }
-    if (owner) owner->reset();
+    timer.end(h);
   }
 };
 
 }  // namespace
 
-const float2* Model::spectra_for(int ci, int T, bool cache) {
-  if (!cache) return nullptr;
+// Kernel spectra are computed at a layer's first use in a forward and kept
+// for the rest of it (every fragment group reuses them); without `cache`
+// they are dropped at the end of the forward, so every forward recomputes them.
+const float2* Model::spectra_for(int ci, int T, bool /*cache*/) {
   auto key = std::make_pair(ci, T);
   auto it = spectra.find(key);
   if (it != spectra.end()) return it->second.as<float2>();
-  // locate the layer of conv ordinal ci
   int64_t f = net.fin;
   for (size_t li = 0; li < net.layers.size(); ++li) {
     const Layer& l = net.layers[li];
@@ -317,12 +332,13 @@ const float2* Model::spectra_for(int ci, int T, bool cache) {
 }
 
 int64_t Model::plan_bytes(const ForwardPlan& p, bool cache) const {
-  PeakModel pm{*this, p, cache};
+  Sched s(*this, p, cache);
   const int64_t in = p.S * entry_bytes(p.shapes[0]);
   const int64_t frags = p.S * p.alpha * entry_bytes(p.shapes.back());
   const int64_t dense = p.S * p.f_out * p.dense.vol() * 4;
   int64_t spectra_bytes = 0;
-  if (cache) {
+  (void)cache;  // spectra are resident for the whole forward either way
+  {
     int64_t f = net.fin;
     for (size_t li = 0; li < net.layers.size(); ++li) {
       const Layer& l = net.layers[li];
@@ -331,23 +347,23 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache) const {
       f = l.fo;
     }
   }
-  // smallest groups: the feasibility threshold
-  const int64_t huge = int64_t(1) << 62;
-  (void)huge;
-  int64_t minimal = 0;
-  {
-    // peak with avail = 0 forces g = 1 at every pool
-    minimal = pm.peak(0, p.S, 0);
-  }
-  return minimal + frags + dense + spectra_bytes + (in - p.S * entry_bytes(p.shapes[0]));
+  return in + frags + dense + spectra_bytes + s.need_min[0];
 }
 
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
                     std::vector<double>* layer_seconds) {
   EventTimer timer(c->stream, layer_seconds != nullptr);
   DevBuf frags(c, p.S * p.alpha * entry_bytes(p.shapes.back()));
-  Runner r{*this, p, cache, frags.as<float>(), 0, timer};
-  r.run(0, d_in, nullptr, p.S);
+  // kernel spectra first, so the group sizes below see their footprint
+  for (size_t li = 0; li < net.layers.size(); ++li)
+    if (net.layers[li].kind == 0 && p.choice[li].algo == VXG_CONV_FFT) {
+      const int h = timer.begin(li);
+      spectra_for(conv_index[li], p.choice[li].fft.T, cache);
+      timer.end(h);
+    }
+  Runner r{*this, p, cache, Sched(*this, p, cache), frags.as<float>(), 0, timer};
+  r.run(0, d_in, p.S);
+  if (!cache) spectra.clear();  // stream-ordered frees: recomputed by the next forward
   const size_t nwin = p.windows.size() / 3;
   if (nwin == 0) {
     VXG_CUDA_CHECK(cudaMemcpyAsync(d_dense, frags.get(), size_t(frags.bytes()),

@@ -57,6 +57,33 @@ struct TileCfg {
 
 constexpr int kFftThreads = 256;
 
+// cp.async (LDGSTS) helpers: asynchronous global -> shared copies that need no
+// registers, so a thread can keep dozens of loads in flight.  pred == false
+// zero-fills the destination (src-size 0).
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// two CTAs per SM whenever the spectrum fits in half the shared memory
+template <int T>
+constexpr int fft_min_blocks() { return T <= 28 ? 2 : 1; }
+
 // ---- K1 / K2: forward tile transform -----------------------------------------
 //
 // One CTA per (tile m, channel j).  A0 stages the real T^3 box (zero outside
@@ -64,7 +91,7 @@ constexpr int kFftThreads = 256;
 // A1 transforms pairs of real z lines with one complex FFT (two-for-one r2c);
 // B / C run the y and x lines in shared memory; D stores the spectrum lines.
 template <int T>
-__global__ void __launch_bounds__(kFftThreads) tile_fwd_kernel(FwdTileArgs a) {
+__global__ void __launch_bounds__(kFftThreads, fft_min_blocks<T>()) tile_fwd_kernel(FwdTileArgs a) {
   using C = TileCfg<T>;
   extern __shared__ float2 sp[];
   float* spf = reinterpret_cast<float*>(sp);
@@ -78,15 +105,19 @@ __global__ void __launch_bounds__(kFftThreads) tile_fwd_kernel(FwdTileArgs a) {
   const int ox = tx * a.vx, oy = ty * a.vy, oz = tz * a.vz;
   const float* img = a.src + (s * a.f + j) * a.img_stride;
 
-  // A0: real box -> slots
+  // A0: real box -> slots, asynchronous 4-byte copies (zero-filled outside
+  // the image) so every thread keeps all of its loads in flight at once
+#pragma unroll 8
   for (int idx = threadIdx.x; idx < T * T * T; idx += kFftThreads) {
     const int z = idx % T, l = idx / T;
     const int y = l % T, x = l / T;
     const int gx = ox + x, gy = oy + y, gz = oz + z;
-    float v = 0.f;
-    if (gx < a.nx && gy < a.ny && gz < a.nz) v = __ldg(img + (int64_t(gx) * a.ny + gy) * a.nz + gz);
-    spf[2 * (x * C::SX + y * C::SY) + z] = v;
+    const bool in = gx < a.nx && gy < a.ny && gz < a.nz;
+    const float* g = in ? img + (int64_t(gx) * a.ny + gy) * a.nz + gz : img;
+    cp_async4(spf + 2 * (x * C::SX + y * C::SY) + z, g, in);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
   // A1: z r2c, lines l and l + T*T/2 share one complex transform
@@ -156,7 +187,7 @@ __global__ void __launch_bounds__(kFftThreads) tile_fwd_kernel(FwdTileArgs a) {
 // z lines (two-for-one c2r) only for (x, y) inside the crop and applies
 // bias + activation; E stores the crop coalesced and clipped to the image.
 template <int T>
-__global__ void __launch_bounds__(kFftThreads) tile_inv_kernel(InvTileArgs a) {
+__global__ void __launch_bounds__(kFftThreads, fft_min_blocks<T>()) tile_inv_kernel(InvTileArgs a) {
   using C = TileCfg<T>;
   extern __shared__ float2 sp[];
   float* spf = reinterpret_cast<float*>(sp);
@@ -168,11 +199,14 @@ __global__ void __launch_bounds__(kFftThreads) tile_inv_kernel(InvTileArgs a) {
   const int64_t t = m % a.tiles_per_img;
   const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
 
-  // A
+  // A: spectrum lines -> smem, asynchronous 8-byte copies
   const float2* src = a.spec + (ml * a.fo + i) * WB;
   const int64_t wb_stride = a.mstride * a.fo * WB;
+#pragma unroll 8
   for (int w = threadIdx.x; w < C::NW; w += kFftThreads)
-    sp[(w / (T * C::H)) * C::SX + w % (T * C::H)] = src[(w / WB) * wb_stride + (w % WB)];
+    cp_async8(sp + (w / (T * C::H)) * C::SX + w % (T * C::H), src + (w / WB) * wb_stride + (w % WB));
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
   // B: x lines, all (ky, kz)
@@ -265,17 +299,6 @@ __global__ void __launch_bounds__(kFftThreads) tile_inv_kernel(InvTileArgs a) {
 // one frequency x MT rows x IT maps (MT*IT complex accumulators, 4 FFMA per
 // complex MAC).  Grid order keeps all m-blocks of one frequency block adjacent
 // so the kernel-spectrum block stays L2-resident while X streams from HBM.
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 template <int MT, int IT, int MB, int IB, int JC>
 struct GemmCfg {

@@ -91,6 +91,114 @@ void dispatch_pool(Ctx* c, const float* in, float* out, const PoolGeom& g) {
     run_pool<0, 0, 0>(c, in, out, g);
 }
 
+// Fast MPF over whole input entries: the dense p-window max filter
+// D[x] = max in[x .. x+p) over x < p*m (per axis), de-interleaved by parity
+// into the P fragments (D[o + p*x'] = fragment o at x').  Every input element
+// is read from HBM once (neighbour reuse through L1) and every output written
+// once.  A thread owns one (y, z) column of D for XT consecutive x and keeps
+// the last PX row maxima in registers.  32-bit index math inside a plane.
+// Output planes may be a channel slice of a wider tensor (f_tot, c0), which
+// the executor uses to pool a conv layer's output channel block by block.
+struct MpfGeom {
+  int nx, ny, nz;       // input extents
+  int mx, my, mz;       // fragment extents
+  int px, py, pz, P;
+  int dx, dy, dz;       // D extents = p * m
+  int f;                // channels of the input planes
+  int f_tot, c0;        // output channel count and offset
+  int tiles_z, tiles_y, tiles_x;
+  int64_t planes;       // S * f
+};
+
+constexpr int MPF_TZ = 32, MPF_TY = 8, MPF_XT = 16;
+
+template <int PX, int PY, int PZ>
+__global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__ in,
+                                                       float* __restrict__ out, MpfGeom g,
+                                                       int* __restrict__ nan_flag) {
+  const int px = PX > 0 ? PX : g.px, py = PY > 0 ? PY : g.py, pz = PZ > 0 ? PZ : g.pz;
+  const int tile = blockIdx.x;
+  const int tz = tile % g.tiles_z, ty = (tile / g.tiles_z) % g.tiles_y, tx = tile / (g.tiles_z * g.tiles_y);
+  const int z = tz * MPF_TZ + threadIdx.x % MPF_TZ;
+  const int y = ty * MPF_TY + threadIdx.x / MPF_TZ;
+  const int x0 = tx * MPF_XT;
+  const int x1 = min(x0 + MPF_XT, g.dx);
+  const bool live = z < g.dz && y < g.dy;
+  bool saw_nan = false;
+  const int64_t nel = int64_t(g.nx) * g.ny * g.nz;
+  const int moel = g.mx * g.my * g.mz;
+  const int zo = z / pz, yo = y / py;
+  const int offyz = (y % py) * pz + (z % pz);
+  for (int64_t plane = blockIdx.y; plane < g.planes; plane += gridDim.y) {
+    if (!live) break;
+    const int64_t s = plane / g.f;
+    const int fm = int(plane % g.f);
+    const float* src = in + plane * nel;
+    float* dst0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(yo) * g.mz + zo;
+    const int64_t fstride = int64_t(g.f_tot) * moel;  // one fragment further
+    if (PX == 2 && PY == 2 && PZ == 2 && x1 - x0 == MPF_XT && z + 1 < g.nz && y + 1 < g.ny) {
+      // hot path: all 4 * (XT + 1) loads issued before any use
+      float v[MPF_XT + 1][4];
+#pragma unroll
+      for (int r = 0; r <= MPF_XT; ++r) {
+        const float* row = src + (int64_t(x0 + r) * g.ny + y) * g.nz + z;
+        v[r][0] = __ldg(row);
+        v[r][1] = __ldg(row + 1);
+        v[r][2] = __ldg(row + g.nz);
+        v[r][3] = __ldg(row + g.nz + 1);
+      }
+      float prev = 0.f;
+#pragma unroll
+      for (int r = 0; r <= MPF_XT; ++r) {
+        float m = v[r][0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          saw_nan |= (v[r][q] != v[r][q]);
+          m = v[r][q] > m ? v[r][q] : m;
+        }
+        saw_nan |= (v[r][0] != v[r][0]);
+        if (r > 0) {
+          const int xd = x0 + r - 1;
+          const float d = m > prev ? m : prev;
+          const int off = (xd & 1) * 4 + offyz;
+          dst0[off * fstride + int64_t(xd >> 1) * g.my * g.mz] = d;
+        }
+        prev = m;
+      }
+      continue;
+    }
+    float r[8];                                       // ring of row maxima (px <= 8)
+    for (int x = x0; x < x1 + px - 1; ++x) {
+      const float* row = src + (int64_t(x) * g.ny + y) * g.nz + z;
+      float m = __ldg(row);
+#pragma unroll
+      for (int qy = 0; qy < py; ++qy)
+#pragma unroll
+        for (int qz = 0; qz < pz; ++qz) {
+          const float v = __ldg(row + qy * g.nz + qz);
+          saw_nan |= (v != v);
+          m = v > m ? v : m;
+        }
+      // shift in; emit D[x - px + 1] once px rows are available
+      if (PX == 2) {
+        r[0] = r[1];
+        r[1] = m;
+      } else {
+        for (int i = 0; i < px - 1; ++i) r[i] = r[i + 1];
+        r[px - 1] = m;
+      }
+      const int xd = x - px + 1;
+      if (xd >= x0) {
+        float d = r[0];
+        for (int i = 1; i < px; ++i) d = r[i] > d ? r[i] : d;
+        const int off = (xd % px) * py * pz + offyz;
+        dst0[off * fstride + int64_t(xd / px) * g.my * g.mz] = d;
+      }
+    }
+  }
+  if (saw_nan) *nan_flag = 1;
+}
+
 __global__ void nan_check_kernel(const float* __restrict__ x, int64_t n, int* flag) {
   bool bad = false;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -143,11 +251,33 @@ __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict_
 
 }  // namespace
 
-void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 b0, i64 nb) {
-  PoolGeom g{n.x, n.y, n.z, n.x / p.x, n.y / p.y, n.z / p.z,
-             int(p.x), int(p.y), int(p.z), int(p.vol()), f, b0, nb};
-  (void)S;
-  dispatch_pool(c, in, out, g);
+void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot,
+                i64 c0) {
+  require(p.x <= 8, "mpf: window above 8 along x");
+  MpfGeom g{};
+  g.nx = int(n.x); g.ny = int(n.y); g.nz = int(n.z);
+  g.mx = int(n.x / p.x); g.my = int(n.y / p.y); g.mz = int(n.z / p.z);
+  g.px = int(p.x); g.py = int(p.y); g.pz = int(p.z); g.P = int(p.vol());
+  g.dx = g.px * g.mx; g.dy = g.py * g.my; g.dz = g.pz * g.mz;
+  g.f = int(f);
+  g.f_tot = int(f_tot > 0 ? f_tot : f);
+  g.c0 = int(c0);
+  g.tiles_z = (g.dz + MPF_TZ - 1) / MPF_TZ;
+  g.tiles_y = (g.dy + MPF_TY - 1) / MPF_TY;
+  g.tiles_x = (g.dx + MPF_XT - 1) / MPF_XT;
+  g.planes = S * f;
+  const int64_t tiles = int64_t(g.tiles_z) * g.tiles_y * g.tiles_x;
+  if (tiles == 0 || g.planes == 0) return;
+  require(tiles < (int64_t(1) << 31), "mpf: grid too large");
+  dim3 grid(unsigned(tiles), unsigned(std::min<int64_t>(g.planes, 65535)));
+  KScope ks(c, VXG_K_POOL, 0.0,
+            4.0 * double(g.planes) * (double(n.x) * n.y * n.z + double(g.P) * g.mx * g.my * g.mz));
+  if (g.px == 2 && g.py == 2 && g.pz == 2)
+    mpf_full_kernel<2, 2, 2><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
+  else
+    mpf_full_kernel<0, 0, 0><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
+  c->counted();
+  check_launch("mpf_full_kernel");
 }
 
 void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out) {

@@ -31,8 +31,10 @@ torch.Tensor is used in place (stream-ordered on the context's stream).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -54,6 +56,25 @@ __all__ = [
 
 # ---- context ---------------------------------------------------------------------------
 
+_live_contexts = weakref.WeakSet()
+_live_models = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all_contexts():
+    # before the CUDA runtime's own teardown at process exit; models first
+    for m in list(_live_models):
+        try:
+            m.close()
+        except Exception:
+            pass
+    for c in list(_live_contexts):
+        try:
+            c.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One per GPU: stream, stream-ordered allocator, HBM budget (bytes; <= 0 = 90% free)."""
 
@@ -62,6 +83,7 @@ class Context:
         check(lib().vxg_ctx_create(int(device), int(budget_bytes), C.byref(p)))
         self._p = p
         self.device = device
+        _live_contexts.add(self)
 
     @property
     def handle(self):
@@ -504,6 +526,7 @@ class Model:
         p = C.c_void_p()
         check(lib().vxg_model_create(self.ctx.handle, net.handle, wi.ptr, wi.mem, C.byref(p)))
         self._p = p
+        _live_models.add(self)
 
     def output_shape(self, S: int, e):
         e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]
