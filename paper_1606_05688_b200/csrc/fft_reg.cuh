@@ -70,6 +70,34 @@ __device__ __forceinline__ void small_dft(float2 (&t)[R]) {
     const float2 a = t[0], b = t[1];
     t[0] = cadd(a, b);
     t[1] = csub(a, b);
+  } else if constexpr (R == 3) {
+    // X0 = x0 + t1, X1/2 = x0 - t1/2 -/+ i s (x1 - x2), s = sin(2 pi / 3) (forward)
+    constexpr float s = 0.866025403784438647f;
+    const float2 t1 = cadd(t[1], t[2]), d = csub(t[1], t[2]);
+    const float2 m = make_float2(fmaf(-0.5f, t1.x, t[0].x), fmaf(-0.5f, t1.y, t[0].y));
+    const float2 r = INV ? make_float2(-s * d.y, s * d.x) : make_float2(s * d.y, -s * d.x);
+    t[0] = cadd(t[0], t1);
+    t[1] = cadd(m, r);
+    t[2] = csub(m, r);
+  } else if constexpr (R == 5) {
+    // Winograd-style 5-point DFT: a_k = x0 + c.(x1+x4) + c'.(x2+x3),
+    // b_k = s.(x1-x4) + s'.(x2-x3); X_k = a_k -/+ i b_k (forward / inverse)
+    constexpr float c1 = 0.309016994374947424f, c2 = -0.809016994374947424f;
+    constexpr float s1 = 0.951056516295153572f, s2 = 0.587785252292473129f;
+    const float2 t1 = cadd(t[1], t[4]), t2 = cadd(t[2], t[3]);
+    const float2 t3 = csub(t[1], t[4]), t4 = csub(t[2], t[3]);
+    const float2 a1 = make_float2(fmaf(c1, t1.x, fmaf(c2, t2.x, t[0].x)), fmaf(c1, t1.y, fmaf(c2, t2.y, t[0].y)));
+    const float2 a2 = make_float2(fmaf(c2, t1.x, fmaf(c1, t2.x, t[0].x)), fmaf(c2, t1.y, fmaf(c1, t2.y, t[0].y)));
+    const float2 b1 = make_float2(fmaf(s1, t3.x, s2 * t4.x), fmaf(s1, t3.y, s2 * t4.y));
+    const float2 b2 = make_float2(fmaf(s2, t3.x, -s1 * t4.x), fmaf(s2, t3.y, -s1 * t4.y));
+    // -i b = (b.y, -b.x); +i b = (-b.y, b.x)
+    const float2 nb1 = INV ? make_float2(-b1.y, b1.x) : make_float2(b1.y, -b1.x);
+    const float2 nb2 = INV ? make_float2(-b2.y, b2.x) : make_float2(b2.y, -b2.x);
+    t[0] = cadd(t[0], cadd(t1, t2));
+    t[1] = cadd(a1, nb1);
+    t[4] = csub(a1, nb1);
+    t[2] = cadd(a2, nb2);
+    t[3] = csub(a2, nb2);
   } else if constexpr (R == 4) {
     const float2 a0 = cadd(t[0], t[2]), a1 = csub(t[0], t[2]);
     const float2 b0 = cadd(t[1], t[3]), b1 = csub(t[1], t[3]);

@@ -1,0 +1,331 @@
+// K1 / K2 / K4: on-chip tile transforms of the tiled pruned-FFT convolution.
+//
+// Math of conv_fft_data_parallel / conv_fft_staged / conv_fft_task_parallel
+// (proj/include/voxin/layers.hpp:203-371, task_conv.hpp:415-442): valid
+// convolution = crop of the circular convolution of zero-padded spectra.  The
+// reference pads the WHOLE image to N(n) and multi-passes every axis through
+// memory; here the output is cut into overlap-save tiles of a cubic FFT size
+// T (T - k + 1 valid outputs per axis per tile), so that
+//   * each 3D transform runs entirely on-chip: one HBM read of the tile box,
+//     one write of its spectrum (K1 tile_fwd_kernel) and the reverse with the
+//     crop, bias and ReLU fused into the store (K4 tile_inv_kernel, pruned to
+//     the lines the crop needs, like pruned_inverse_region, fft.hpp:181-228);
+//   * kernel spectra are small (T^3), computed once per layer by the same
+//     forward kernel on the zero-filled k^3 kernels (K2) and pre-scaled by
+//     1/T^3, so the inverse needs no normalisation pass.
+// Spectra live in HBM as [w/16][row][channel][w%16] complex64 so every
+// producer and consumer moves whole 128-byte lines; w = (kx*T + ky)*H + kz.
+//
+// Shared-memory layout: line (x, y) of z values lives in a slot of SY >= H
+// complex (SY odd, so the slot-per-lane passes are bank-conflict free);
+// x planes are SX apart with SX = H (mod 16) so the y-line pass is conflict
+// free too.  One CTA owns one (tile, channel); every pass gives each thread
+// exactly one register-resident line (THREADS = T*H rounded up to a warp).
+#include <cmath>
+#include <vector>
+
+#include "async.cuh"
+#include "common.cuh"
+#include "fft_reg.cuh"
+#include "fftconv.hpp"
+
+namespace vxg {
+
+void init_twiddles() {
+  std::vector<float2> h(fftreg::kTwTotal);
+  for (int i = 0; i < fftreg::kNumSizes; ++i) {
+    const int n = fftreg::kSizes[i];
+    const int off = fftreg::tw_offset(n);
+    for (int t = 0; t < n; ++t) {
+      const double a = -2.0 * M_PI * double(t) / double(n);  // unit_roots, dft.hpp:39-47
+      h[off + t] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+  }
+  VXG_CUDA_CHECK(cudaMemcpyToSymbol(c_twiddle, h.data(), sizeof(float2) * h.size()));
+}
+
+namespace {
+
+template <int T>
+struct TileCfg {
+  static constexpr int H = T / 2 + 1;                       // halved z extent
+  static constexpr int SY = H | 1;                          // slot stride (odd)
+  static constexpr int PADX = ((H - (T * SY) % 16) % 16 + 16) % 16;
+  static constexpr int SX = T * SY + PADX;                  // x-plane stride
+  static constexpr int NW = T * T * H;                      // frequencies per tile
+  static constexpr int NWB = (NW + WB - 1) / WB;
+  static constexpr int SMEM = T * SX * 8;                   // bytes
+  static constexpr int THREADS = ((T * H + 31) / 32) * 32;  // one line per thread per pass
+  static constexpr int MINB = T >= 28 ? 1 : (T >= 24 ? 2 : (T >= 20 ? 3 : 4));
+  static __device__ __forceinline__ int idx(int kx, int ky, int kz) { return kx * SX + ky * SY + kz; }
+};
+
+// ---- K1 / K2: forward tile transform -----------------------------------------
+template <int T>
+__global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
+    tile_fwd_kernel(FwdTileArgs a) {
+  using C = TileCfg<T>;
+  extern __shared__ float2 sp[];
+  float* spf = reinterpret_cast<float*>(sp);
+  const int64_t blk = blockIdx.x;
+  const int64_t j = blk % a.f;
+  const int64_t ml = blk / a.f;
+  const int64_t m = a.m0 + ml;
+  const int64_t s = m / a.tiles_per_img;
+  const int64_t t = m % a.tiles_per_img;
+  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
+  const int ox = tx * a.vx, oy = ty * a.vy, oz = tz * a.vz;
+  const float* img = a.src + (s * a.f + j) * a.img_stride;
+  const int tid = threadIdx.x;
+
+  // A0: real box -> slots (asynchronous 4-byte copies, zero outside the image)
+#pragma unroll 4
+  for (int idx = tid; idx < T * T * T; idx += C::THREADS) {
+    const int z = idx % T, l = idx / T;
+    const int y = l % T, x = l / T;
+    const int gx = ox + x, gy = oy + y, gz = oz + z;
+    const bool in = gx < a.nx && gy < a.ny && gz < a.nz;
+    const float* g = in ? img + (int64_t(gx) * a.ny + gy) * a.nz + gz : img;
+    cp_async4(spf + 2 * (x * C::SX + y * C::SY) + z, g, in);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // A1: z r2c, lines l and l + T*T/2 share one complex transform (two-for-one)
+  constexpr int LH = T * T / 2;
+  if (tid < LH) {
+    const int l1 = tid, l2 = tid + LH;
+    float2* s1 = sp + (l1 / T) * C::SX + (l1 % T) * C::SY;
+    float2* s2 = sp + (l2 / T) * C::SX + (l2 % T) * C::SY;
+    float2 zz[T];
+#pragma unroll
+    for (int q = 0; q < T / 2; ++q) {
+      const float2 r1 = s1[q], r2 = s2[q];
+      zz[2 * q] = make_float2(r1.x, r2.x);
+      zz[2 * q + 1] = make_float2(r1.y, r2.y);
+    }
+    fft<T, false>(zz);
+#pragma unroll
+    for (int k = 0; k < C::H; ++k) {
+      const float2 zk = zz[k];
+      const float2 zn = cconj(zz[(T - k) % T]);
+      const float2 d = csub(zk, zn);
+      s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
+      s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
+    }
+  }
+  __syncthreads();
+
+  // B: y lines (x, kz)
+  if (tid < T * C::H) {
+    const int kz = tid % C::H, x = tid / C::H;
+    float2* base = sp + x * C::SX + kz;
+    float2 v[T];
+#pragma unroll
+    for (int y = 0; y < T; ++y) v[y] = base[y * C::SY];
+    fft<T, false>(v);
+#pragma unroll
+    for (int y = 0; y < T; ++y) base[y * C::SY] = v[y];
+  }
+  __syncthreads();
+
+  // C: x lines (ky, kz), with the output scale
+  if (tid < T * C::H) {
+    const int kz = tid % C::H, ky = tid / C::H;
+    float2* base = sp + ky * C::SY + kz;
+    float2 v[T];
+#pragma unroll
+    for (int x = 0; x < T; ++x) v[x] = base[x * C::SX];
+    fft<T, false>(v);
+#pragma unroll
+    for (int x = 0; x < T; ++x) base[x * C::SX] = make_float2(v[x].x * a.scale, v[x].y * a.scale);
+  }
+  __syncthreads();
+
+  // D: spectrum lines, zero tail up to NWB*16
+  float2* dst = a.out + (ml * a.f + j) * WB;
+  const int64_t wb_stride = a.mstride * a.f * WB;
+  for (int w = tid; w < C::NWB * WB; w += C::THREADS) {
+    float2 v = make_float2(0.f, 0.f);
+    if (w < C::NW) {
+      const int kx = w / (T * C::H), r = w % (T * C::H);
+      v = sp[C::idx(kx, r / C::H, r % C::H)];
+    }
+    dst[(w / WB) * wb_stride + (w % WB)] = v;
+  }
+}
+
+// ---- K4: inverse tile transform with crop + bias + ReLU ------------------------
+template <int T>
+__global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
+    tile_inv_kernel(InvTileArgs a) {
+  using C = TileCfg<T>;
+  extern __shared__ float2 sp[];
+  float* spf = reinterpret_cast<float*>(sp);
+  const int64_t blk = blockIdx.x;
+  const int64_t i = blk % a.fo;
+  const int64_t ml = blk / a.fo;
+  const int64_t m = a.m0 + ml;
+  const int64_t s = m / a.tiles_per_img;
+  const int64_t t = m % a.tiles_per_img;
+  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
+  const int tid = threadIdx.x;
+
+  // A: spectrum lines -> smem (asynchronous 8-byte copies)
+  const float2* src = a.spec + (ml * a.fo + i) * WB;
+  const int64_t wb_stride = a.mstride * a.fo * WB;
+#pragma unroll 4
+  for (int w = tid; w < C::NW; w += C::THREADS) {
+    const int kx = w / (T * C::H), r = w % (T * C::H);
+    cp_async8(sp + C::idx(kx, r / C::H, r % C::H), src + (w / WB) * wb_stride + (w % WB));
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // B: x lines, all (ky, kz)
+  if (tid < T * C::H) {
+    const int kz = tid % C::H, ky = tid / C::H;
+    float2* base = sp + ky * C::SY + kz;
+    float2 v[T];
+#pragma unroll
+    for (int x = 0; x < T; ++x) v[x] = base[x * C::SX];
+    fft<T, true>(v);
+#pragma unroll
+    for (int x = 0; x < T; ++x) base[x * C::SX] = v[x];
+  }
+  __syncthreads();
+
+  // C: y lines only for x inside the crop
+  if (tid < a.vx * C::H) {
+    const int kz = tid % C::H, x = a.cx + tid / C::H;
+    float2* base = sp + x * C::SX + kz;
+    float2 v[T];
+#pragma unroll
+    for (int y = 0; y < T; ++y) v[y] = base[y * C::SY];
+    fft<T, true>(v);
+#pragma unroll
+    for (int y = 0; y < T; ++y) base[y * C::SY] = v[y];
+  }
+  __syncthreads();
+
+  // D: z c2r for (x, y) inside the crop, pairs (l, l + half); bias + activation
+  const int L = a.vx * a.vy;
+  const int half = (L + 1) / 2;
+  if (tid < half) {
+    const float bias = __ldg(a.bias + i);
+    const int l1 = tid, l2 = tid + half;
+    const bool has2 = l2 < L;
+    float2* s1 = sp + (a.cx + l1 / a.vy) * C::SX + (a.cy + l1 % a.vy) * C::SY;
+    float2* s2 = has2 ? sp + (a.cx + l2 / a.vy) * C::SX + (a.cy + l2 % a.vy) * C::SY : s1;
+    float2 zz[T];
+#pragma unroll
+    for (int k = 0; k < C::H; ++k) {
+      const float2 A = s1[k];
+      const float2 B = has2 ? s2[k] : make_float2(0.f, 0.f);
+      zz[k] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
+    }
+#pragma unroll
+    for (int k = C::H; k < T; ++k) {
+      const float2 A = s1[T - k];
+      const float2 B = has2 ? s2[T - k] : make_float2(0.f, 0.f);
+      zz[k] = make_float2(A.x + B.y, -A.y + B.x);  // conj(A) + i conj(B)
+    }
+    fft<T, true>(zz);
+    float* r1 = spf + 2 * (s1 - sp);
+    float* r2 = spf + 2 * (s2 - sp);
+#pragma unroll
+    for (int z = 0; z < T; ++z) {
+      if (z >= a.cz && z < a.cz + a.vz) {
+        const float v1 = zz[z].x + bias;
+        r1[z] = a.relu ? (v1 > 0.f ? v1 : 0.f) : v1;  // activate (layers.hpp:105-108)
+        if (has2) {
+          const float v2 = zz[z].y + bias;
+          r2[z] = a.relu ? (v2 > 0.f ? v2 : 0.f) : v2;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // E: coalesced store of the crop, clipped to the output image
+  float* out = a.dst + (s * a.fo + i) * a.oel;
+  const int gx0 = tx * a.vx, gy0 = ty * a.vy, gz0 = tz * a.vz;
+  const int V = a.vx * a.vy * a.vz;
+  for (int idx = tid; idx < V; idx += C::THREADS) {
+    const int z = idx % a.vz, l = idx / a.vz;
+    const int y = l % a.vy, x = l / a.vy;
+    const int gx = gx0 + x, gy = gy0 + y, gz = gz0 + z;
+    if (gx < a.onx && gy < a.ony && gz < a.onz)
+      out[(int64_t(gx) * a.ony + gy) * a.onz + gz] =
+          spf[2 * ((a.cx + x) * C::SX + (a.cy + y) * C::SY) + a.cz + z];
+  }
+}
+
+template <int T>
+void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
+  using C = TileCfg<T>;
+  static bool configured = false;
+  if (!configured) {
+    VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_kernel<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  tile_fwd_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
+  c->counted();
+  check_launch("tile_fwd_kernel");
+}
+
+template <int T>
+void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
+  using C = TileCfg<T>;
+  static bool configured = false;
+  if (!configured) {
+    VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_kernel<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  tile_inv_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
+  c->counted();
+  check_launch("tile_inv_kernel");
+}
+
+}  // namespace
+
+// supported tile FFT sizes (even, {2,3,5,7}-smooth)
+const int kTileSizes[] = {4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32};
+const int kNumTileSizes = sizeof(kTileSizes) / sizeof(int);
+
+int64_t tile_nwb(int T) { return (int64_t(T) * T * (T / 2 + 1) + WB - 1) / WB; }
+
+#define VXG_TILE_SWITCH(FN)                                         \
+  switch (T) {                                                      \
+    case 4: FN<4>(c, a, nblocks); break;                            \
+    case 6: FN<6>(c, a, nblocks); break;                            \
+    case 8: FN<8>(c, a, nblocks); break;                            \
+    case 10: FN<10>(c, a, nblocks); break;                          \
+    case 12: FN<12>(c, a, nblocks); break;                          \
+    case 16: FN<16>(c, a, nblocks); break;                          \
+    case 20: FN<20>(c, a, nblocks); break;                          \
+    case 24: FN<24>(c, a, nblocks); break;                          \
+    case 28: FN<28>(c, a, nblocks); break;                          \
+    case 30: FN<30>(c, a, nblocks); break;                          \
+    case 32: FN<32>(c, a, nblocks); break;                          \
+    default: throw invalid("tile fft: unsupported tile size");      \
+  }
+
+void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks) {
+  const double nw = double(T) * T * (T / 2 + 1);
+  KScope ks(c, a.kind, 0.0, double(nblocks) * (4.0 * double(T) * T * T + 8.0 * nw));
+  VXG_TILE_SWITCH(fwd_t)
+}
+
+void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a, int64_t nblocks) {
+  const double nw = double(T) * T * (T / 2 + 1);
+  KScope ks(c, VXG_K_TILE_INV, 0.0,
+            double(nblocks) * (8.0 * nw + 4.0 * double(a.vx) * a.vy * a.vz));
+  VXG_TILE_SWITCH(inv_t)
+}
+
+}  // namespace vxg

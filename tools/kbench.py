@@ -39,20 +39,25 @@ def main():
     ap.add_argument("--which", default="conv,direct,mpf")
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--T", type=int, default=0)
+    ap.add_argument("--S", type=int, default=1)
     a = ap.parse_args()
     ctx = v.Context(0)
     res = {}
     g = torch.Generator(device="cuda").manual_seed(1)
     if "conv" in a.which:
         n = a.n
-        x = torch.rand((1, 80, n, n, n), device="cuda", generator=g) * 2 - 1
+        x = torch.rand((a.S, 80, n, n, n), device="cuda", generator=g) * 2 - 1
         w = (torch.rand((80, 80, 5, 5, 5), device="cuda", generator=g) * 2 - 1) * 0.02
         b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
         p = v.ConvLayerParams(w, b, "relu")
+        ctx.profile(True)
         t = timed(ctx, lambda: v.conv_fft_staged(x, p, ctx))
+        ks = ctx.kernel_stats()
+        ctx.profile(False)
         no = n - 4
-        flops = 8.0 * 80 * 80 * (n ** 3) * 0  # placeholder
-        res["conv_fft_80x80_k5_n%d" % n] = {"s": t, "vox_per_s": no ** 3 / t}
+        res["conv_fft_80x80_k5_S%d_n%d" % (a.S, n)] = {
+            "s": t, "vox_per_s": a.S * no ** 3 / t,
+            "kernels": {k: round(s["seconds"] / s["launches"] * 1e3, 3) for k, s in ks.items()}}
         del x
     if "direct" in a.which:
         n = 330
