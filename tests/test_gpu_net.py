@@ -100,3 +100,40 @@ def test_forward_errors(ctx):
     with pytest.raises(v.ResourceExhausted):
         v.execute(net, w, np.zeros((1, 1, 148, 148, 148), np.float32), tiny)
     tiny.close()
+
+
+def test_cpp_dropin_runs_bundled_net_unchanged(golden, tmp_path):
+    """A reference-style C++ caller (include/voxin_b200.hpp) runs the bundled
+    n337 description through parse -> random_weights -> execute."""
+    import subprocess
+    from conftest import ROOT
+    meta = json.loads((GOLD / "nets_bundled.json").read_text())["n337"]
+    exe = tmp_path / "shim_net"
+    lib = ROOT / "paper_1606_05688_b200"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "cpp" / "shim_net.cpp"), "-L", str(lib), "-lvxg",
+                    f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    net_file = tmp_path / "n337.net"
+    net_file.write_text(meta["text"])
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(net_file), str(meta["extent"][0]), str(meta["wseed"]),
+                        str(meta["iseed"]), str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
+    got = np.fromfile(out, np.float32).reshape(meta["out_shape"])
+    assert rel_error(got, golden("nets_bundled")["n337_out64"]) <= TOL
+
+
+def test_tiled_volume_equals_whole_volume(ctx):
+    """Halo tiles (the multi-GPU sharding unit) stitch to the whole-volume output."""
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200 import tiler
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    model = v.Model(net, v.random_weights(net, 5), ctx)
+    vol = v.fill_random((1, 1, 140, 132, 124), 17)
+    dense = tiler.infer_volume(model, vol, (24, 24, 16))
+    # reference: each 8-aligned output block from one big forward of the largest admissible crop
+    full, _ = model.forward(np.ascontiguousarray(vol[:, :, :132, :132, :124]))
+    assert dense.shape == (1, 3, 56, 48, 40)
+    err = np.abs(dense[:, :, :48, :48, :40] - full).max() / np.abs(full).max()
+    assert err <= TOL, err

@@ -1,0 +1,101 @@
+"""CPU: the N>1 host logic -- halo tiling, round-robin rank assignment, resume,
+and the point-to-point gather to rank 0 -- across world_size 2 with the gloo
+backend.  A numpy stand-in with a known field of view replaces the network
+(the tiler only relies on translation equivariance)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1606_05688_b200 import tiler
+
+
+def box_net(x, fov):
+    """dense out[d] = sum(in[d : d + fov]) per axis (a translation-equivariant 'net')."""
+    c = np.cumsum(np.cumsum(np.cumsum(x, axis=2), axis=3), axis=4)
+    c = np.pad(c, ((0, 0), (0, 0), (1, 0), (1, 0), (1, 0)))
+    f = fov
+    s = (c[:, :, f:, f:, f:] - c[:, :, :-f, f:, f:] - c[:, :, f:, :-f, f:] - c[:, :, f:, f:, :-f]
+         + c[:, :, :-f, :-f, f:] + c[:, :, :-f, f:, :-f] + c[:, :, f:, :-f, :-f]
+         - c[:, :, :-f, :-f, :-f])
+    return s.astype(np.float32)
+
+
+def test_plan_tiles_cover_output_exactly_once():
+    vol, fov = (50, 41, 37), (7, 7, 7)
+    tiles = tiler.plan_tiles(vol, fov, (16, 16, 16), (4, 4, 4))
+    dense = [vol[a] - fov[a] + 1 for a in range(3)]
+    cover = np.zeros(dense, np.int32)
+    for t in tiles:
+        assert all(t.in_extent[a] == t.out_extent[a] + fov[a] - 1 for a in range(3))
+        assert all(e % 4 == 0 for e in t.out_extent)
+        assert all(t.in_origin[a] + t.in_extent[a] <= vol[a] for a in range(3))
+        sl = tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a]) for a in range(3))
+        cover[sl] += 1
+    assert (cover == 1).all()
+    mine = [tiler.assign(tiles, r, 3) for r in range(3)]
+    assert sorted(t.index for m in mine for t in m) == list(range(len(tiles)))
+
+
+def test_run_tiles_matches_full_and_resumes():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((1, 2, 40, 33, 29)).astype(np.float32)
+    fov = 6
+    full = box_net(x, fov)
+    tiles = tiler.plan_tiles(x.shape[2:], (fov,) * 3, (12, 12, 12))
+    out = np.zeros_like(full)
+    done = set()
+    tiler.run_tiles(lambda c: box_net(c, fov), x, tiles[: len(tiles) // 2], out, done)
+    calls = []
+
+    def counting(c):
+        calls.append(1)
+        return box_net(c, fov)
+
+    tiler.run_tiles(counting, x, tiles, out, done)  # resume: finished tiles are skipped
+    assert len(calls) == len(tiles) - len(tiles) // 2
+    np.testing.assert_allclose(out, full, rtol=1e-5, atol=1e-4)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, 1, 36, 30, 34)).astype(np.float32)
+    fov = 5
+    tiles = tiler.plan_tiles(x.shape[2:], (fov,) * 3, (8, 8, 8), (2, 2, 2))
+    mine = tiler.assign(tiles, rank, world)
+    blocks = tiler.run_tiles(lambda c: box_net(c, fov), x, mine)
+    dense = tuple(x.shape[2 + a] - fov + 1 for a in range(3))
+    out = np.zeros((1, 1) + dense, np.float32) if rank == 0 else None
+    tiler.gather_to_root(blocks, tiles, out, 1, device="cpu")
+    # timing reduction of the bench: max over ranks
+    import torch
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        q.put((np.abs(out - box_net(x, fov)).max(), t.item(), len(mine)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_gloo():
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    err, tmax, n0 = q.get(timeout=10)
+    assert err < 1e-3
+    assert tmax == 2.0
+    assert n0 > 0
