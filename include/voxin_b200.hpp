@@ -150,6 +150,8 @@ inline LayerResult<float> conv(int algo, Tensor5<float> in, const ConvLayerParam
   const i64 n[3] = {s.n.x, s.n.y, s.n.z}, k[3] = {ks.n.x, ks.n.y, ks.n.z};
   if (ks.f != s.f) throw std::invalid_argument("conv: kernel feature count mismatch");
   if (static_cast<i64>(p.bias.size()) != ks.s) throw std::invalid_argument("conv: bias count mismatch");
+  if (k[0] > n[0] || k[1] > n[1] || k[2] > n[2])
+    throw std::invalid_argument("conv: kernel larger than image");  // layers.hpp:32
   Tensor5<float> out(Shape5{s.s, ks.s, {n[0] - k[0] + 1, n[1] - k[1] + 1, n[2] - k[2] + 1}});
   vxg_audit au{};
   vxg_throw(vxg_conv(d.get(), algo, VXG_MEM_HOST, in.data(), s.s, s.f, n, p.kernels.data(), ks.s, k,

@@ -293,9 +293,10 @@ int vxg_conv(vxg_ctx* ctx, int algo, int mem, const float* in, int64_t S, int64_
     double model = 0;
     if (use_fft) {
       conv_fft_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p, plan, nullptr, 0);
+      // in + out + kernel spectra + the spectrum chunk buffers actually used
       const int64_t M = S * plan.tiles;
-      model = double(S * f * n.vol() + S * fo * no.vol() + plan.nwb * fo * f * 32 +
-                     std::min<int64_t>(M, 1) * 0) ;
+      model = double(S * f * n.vol() + S * fo * no.vol()) +
+              2.0 * double(plan.nwp) * double(fo * f + M * (f + fo));
     } else {
       conv_direct_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p);
       model = double(S * f * n.vol() + S * fo * no.vol());

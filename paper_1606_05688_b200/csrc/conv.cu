@@ -5,14 +5,25 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 
 #include "fftconv.hpp"
 
 namespace vxg {
 
+namespace {
+
+// VXG_NO_TC=1 pins the fp32 FFMA contraction (parity cross-checks, A/B timing)
+bool tc_disabled() {
+  const char* e = std::getenv("VXG_NO_TC");
+  return e && std::strcmp(e, "0") != 0;
+}
+
+}  // namespace
+
 int64_t fft_chunk_bytes(const FftPlan& plan, int64_t f, int64_t fo, int64_t rows) {
-  return rows * (f + fo) * plan.nwb * 16 * 8;
+  return rows * (f + fo) * plan.nwp * 8;
 }
 
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
@@ -26,6 +37,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
       if (t >= k.x && t >= k.y && t >= k.z) T_forced = t;
     }
   }
+  const bool tc = cgemm_tc_supported(f, fo) && !tc_disabled();
   for (int ti = 0; ti < kNumTileSizes; ++ti) {
     const int T = kTileSizes[ti];
     if (T_forced > 0 && T != T_forced) continue;
@@ -37,24 +49,40 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
       p.nt[a] = (no[a] + p.v[a] - 1) / p.v[a];
     }
     p.tiles = p.nt.vol();
-    p.nwb = tile_nwb(T);
+    p.lw = 16;
+    p.tc = tc;
+    p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);
-    const double nw = double(p.nwb) * 16.0;
-    // modelled seconds: contraction at ~50 TFLOP/s fp32, spectrum + image
-    // traffic at ~5 TB/s, and a per-CTA transform overhead
+    const double nw = double(T) * T * (T / 2 + 1);
+    // Modelled seconds (calibrated on B200 with tools/kbench.py): the
+    // contraction at ~40 TFLOP/s (FFMA) or ~150 TFLOP/s (tcgen05), the
+    // transforms at ~140 ns per (tile, channel) CTA for T = 32 scaling with
+    // T^3 log T, and the spectrum round trips at ~5 TB/s.
     const double flops = 8.0 * M * double(f) * double(fo) * nw;
-    const double bytes = M * (double(f) * (double(T) * T * T * 4.0 + 3.0 * nw * 8.0) +
-                              double(fo) * (3.0 * nw * 8.0 + double(p.v.vol()) * 4.0));
-    const double ctas = M * double(f + fo);
-    p.cost = flops / 50e12 + bytes / 5e12 + ctas * (double(T) * T * T) * 2e-14 * std::log2(double(T));
+    const double cta = 140e-9 * std::pow(double(T) / 32.0, 3.0) * std::log2(double(T)) / 5.0;
+    const double bytes = 16.0 * M * double(f + fo) * nw;
+    p.cost = flops / (tc ? 150e12 : 40e12) + M * double(f + fo) * cta + bytes / 5e12;
     if (p.cost < best.cost) best = p;
   }
   if (best.T == 0) throw invalid("conv fft: no supported tile size covers the kernel");
   return best;
 }
 
-void compute_kernel_spectra(Ctx* c, int T, const float* w, int64_t fo, int64_t f, V3 k,
+int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo) {
+  if (plan.tc) return tc_wsplit_bytes(plan.nwp / 2, f, fo);
+  return plan.nwp * fo * f * 8;
+}
+
+// tc: the raw spectra go through a scratch buffer and are stored pre-split
+// for the tensor cores (tc_wsplit); otherwise raw into `out`.
+void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, int64_t f, V3 k,
                             float2* out) {
+  DevBuf raw;
+  float2* dst = out;
+  if (tc) {
+    raw.alloc(c, tile_nwp(T, 16) * fo * f * 8);
+    dst = raw.as<float2>();
+  }
   FwdTileArgs a{};
   a.src = w;
   a.img_stride = k.vol();
@@ -65,10 +93,12 @@ void compute_kernel_spectra(Ctx* c, int T, const float* w, int64_t fo, int64_t f
   a.f = f;
   a.m0 = 0;
   a.mstride = fo;
-  a.out = out;
+  a.out = dst;
   a.scale = float(1.0 / (double(T) * double(T) * double(T)));
   a.kind = VXG_K_KSPEC;
+  a.lw = 16;
   launch_tile_fwd(c, T, a, fo * f);
+  if (tc) tc_wsplit(c, dst, out, tile_nwp(T, 16) / 2, f, fo);
 }
 
 void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
@@ -78,8 +108,8 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
   const int T = plan.T;
   DevBuf wbuf;
   if (!wspec) {
-    wbuf.alloc(c, plan.nwb * fo * f * 16 * 8);
-    compute_kernel_spectra(c, T, w, fo, f, k, wbuf.as<float2>());
+    wbuf.alloc(c, kernel_spectra_bytes(plan, f, fo));
+    compute_kernel_spectra(c, T, plan.tc, w, fo, f, k, wbuf.as<float2>());
     wspec = wbuf.as<float2>();
   }
   const int64_t M = S * plan.tiles;
@@ -92,8 +122,8 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
   int64_t rows = std::max<int64_t>(1, avail / per_row);
   rows = std::min(rows, M);
   rows = std::min<int64_t>(rows, ((int64_t(1) << 31) - 1) / std::max(f, fo));
-  DevBuf X(c, rows * f * plan.nwb * 16 * 8);
-  DevBuf Y(c, rows * fo * plan.nwb * 16 * 8);
+  DevBuf X(c, rows * f * plan.nwp * 8);
+  DevBuf Y(c, rows * fo * plan.nwp * 8);
 
   for (int64_t m0 = 0; m0 < M; m0 += rows) {
     const int64_t mc = std::min(rows, M - m0);
@@ -109,6 +139,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     fa.mstride = rows;
     fa.out = X.as<float2>();
     fa.scale = 1.f;
+    fa.lw = plan.lw;
     launch_tile_fwd(c, T, fa, mc * f);
 
     GemmArgs ga{};
@@ -120,7 +151,10 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ga.f = int(f);
     ga.fo = int(fo);
     ga.T = T;
-    launch_cgemm(c, ga, plan.nwb);
+    if (plan.tc)
+      launch_cgemm_tc(c, ga, plan.nwp / 2);
+    else
+      launch_cgemm(c, ga, plan.nwp / 16);
 
     InvTileArgs ia{};
     ia.spec = Y.as<float2>();
@@ -136,6 +170,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ia.m0 = m0;
     ia.bias = bias;
     ia.relu = relu ? 1 : 0;
+    ia.lw = plan.lw;
     launch_tile_inv(c, T, ia, mc * fo);
   }
 }

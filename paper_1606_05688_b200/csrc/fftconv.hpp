@@ -18,9 +18,10 @@ struct FwdTileArgs {
   int64_t f;                 // channels per batch entry
   int64_t m0;                // first (batch, tile) row of this launch
   int64_t mstride;           // rows of the spectrum buffer (layout stride)
-  float2* out;               // [w/16][mstride][f][16]
+  float2* out;               // [w/lw][mstride][f][lw]
   float scale;
   int kind = VXG_K_TILE_FWD; // instrumentation family (images or kernel spectra)
+  int lw = 16;               // frequencies per contiguous chunk (16: FFMA path, 2: tensor cores)
 };
 
 struct InvTileArgs {
@@ -37,6 +38,7 @@ struct InvTileArgs {
   int64_t m0;
   const float* bias;
   int relu;
+  int lw = 16;
 };
 
 struct GemmArgs {
@@ -48,15 +50,22 @@ struct GemmArgs {
   int f, fo;
   int mblocks, iblocks;
   int T;                     // tile size (for the algorithmic flop count)
+  int64_t npairs;            // tensor-core path: frequency pairs
 };
 
 extern const int kTileSizes[];
 extern const int kNumTileSizes;
-int64_t tile_nwb(int T);
+// frequencies of a T^3 tile padded to a multiple of the chunk width lw
+int64_t tile_nwp(int T, int lw);
 void init_twiddles();
 void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks);
 void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a, int64_t nblocks);
-void launch_cgemm(Ctx* c, const GemmArgs& a, int64_t nwb);
+void launch_cgemm(Ctx* c, const GemmArgs& a, int64_t nwb);          // FFMA, lw = 16
+bool cgemm_tc_supported(int64_t f, int64_t fo);
+void launch_cgemm_tc(Ctx* c, const GemmArgs& a, int64_t npairs);    // tcgen05, lw = 2
+// pre-split (tf32 hi/lo, UMMA layout) kernel spectra for the tensor-core path
+int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
+void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
 
 // Tile-size choice for a layer: minimises the modelled cost of transforms +
 // contraction over the supported sizes (or honours T_forced > 0).
@@ -65,14 +74,18 @@ struct FftPlan {
   V3 v;        // valid outputs per tile per axis
   V3 nt;       // tiles per axis
   int64_t tiles = 0;
-  int64_t nwb = 0;
+  int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
+  bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
+  int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced = 0);
 
-// Device kernel spectra of one layer for tile size T: [nwb][fo][f][16], scaled 1/T^3.
-void compute_kernel_spectra(Ctx* c, int T, const float* w, int64_t fo, int64_t f, V3 k,
+// Device kernel spectra of one layer for tile size T: [w/lw][fo][f][lw], scaled 1/T^3.
+void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, int64_t f, V3 k,
                             float2* out);
+// bytes of one layer's device kernel spectra in the layout plan.lw selects
+int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo);
 
 // Conv layer drivers on device pointers.  `wspec` (optional) are cached kernel
 // spectra for plan.T; otherwise computed into scratch.  spectra_budget bounds

@@ -291,7 +291,7 @@ struct Runner {
     if (l.kind == 0) {
       const int ci = m.conv_index[li];
       if (p.choice[li].algo == VXG_CONV_FFT) {
-        const float2* ws = m.spectra_for(ci, p.choice[li].fft.T, cache);
+        const float2* ws = m.spectra_for(ci, p.choice[li].fft, cache);
         conv_fft_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
                         m.bias[size_t(ci)].as<float>(), l.relu, dst, p.choice[li].fft, ws, 0);
       } else {
@@ -312,8 +312,9 @@ struct Runner {
 // Kernel spectra are computed at a layer's first use in a forward and kept
 // for the rest of it (every fragment group reuses them); without `cache`
 // they are dropped at the end of the forward, so every forward recomputes them.
-const float2* Model::spectra_for(int ci, int T, bool /*cache*/) {
-  auto key = std::make_pair(ci, T);
+const float2* Model::spectra_for(int ci, const FftPlan& plan, bool /*cache*/) {
+  const int T = plan.T;
+  auto key = std::make_pair(ci, (T << 8) | (plan.tc ? 1 : 0));
   auto it = spectra.find(key);
   if (it != spectra.end()) return it->second.as<float2>();
   int64_t f = net.fin;
@@ -321,8 +322,9 @@ const float2* Model::spectra_for(int ci, int T, bool /*cache*/) {
     const Layer& l = net.layers[li];
     if (l.kind != 0) continue;
     if (conv_index[li] == ci) {
-      DevBuf b(c, tile_nwb(T) * l.fo * f * 16 * 8);
-      compute_kernel_spectra(c, T, kern[size_t(ci)].as<float>(), l.fo, f, l.ext, b.as<float2>());
+      DevBuf b(c, kernel_spectra_bytes(plan, f, l.fo));
+      compute_kernel_spectra(c, T, plan.tc, kern[size_t(ci)].as<float>(), l.fo, f, l.ext,
+                             b.as<float2>());
       auto res = spectra.emplace(key, std::move(b));
       return res.first->second.as<float2>();
     }
@@ -343,7 +345,7 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache) const {
     for (size_t li = 0; li < net.layers.size(); ++li) {
       const Layer& l = net.layers[li];
       if (l.kind != 0) continue;
-      if (p.choice[li].algo == VXG_CONV_FFT) spectra_bytes += p.choice[li].fft.nwb * l.fo * f * 128;
+      if (p.choice[li].algo == VXG_CONV_FFT) spectra_bytes += kernel_spectra_bytes(p.choice[li].fft, f, l.fo);
       f = l.fo;
     }
   }
@@ -358,7 +360,7 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
   for (size_t li = 0; li < net.layers.size(); ++li)
     if (net.layers[li].kind == 0 && p.choice[li].algo == VXG_CONV_FFT) {
       const int h = timer.begin(li);
-      spectra_for(conv_index[li], p.choice[li].fft.T, cache);
+      spectra_for(conv_index[li], p.choice[li].fft, cache);
       timer.end(h);
     }
   Runner r{*this, p, cache, Sched(*this, p, cache), frags.as<float>(), 0, timer};

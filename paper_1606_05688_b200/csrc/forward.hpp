@@ -45,7 +45,7 @@ struct Model {
   // layer_seconds (optional) gets per-layer device time
   void forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache_spectra,
                std::vector<double>* layer_seconds);
-  const float2* spectra_for(int ci, int T, bool cache);
+  const float2* spectra_for(int ci, const FftPlan& plan, bool cache);
 };
 
 }  // namespace vxg

@@ -1,0 +1,430 @@
+// K3 on the 5th-generation tensor cores: the per-frequency complex
+// contraction Y[w](m, i) = sum_j X[w](m, j) W[w](i, j) (the MAC of
+// proj/include/voxin/layers.hpp:245-251, 330-344) as tcgen05.mma kind::tf32
+// with a 3xTF32 split (a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi, fp32
+// accumulation in TMEM), which keeps fp32-level accuracy (~2^-21 relative per
+// product) inside the 1e-4 parity tolerance.
+//
+// Complex -> real: for each frequency w, with X = Xr + i Xi and W = Wr + i Wi,
+//   Dr += Xr Wr^T - Xi Wi^T      (the minus via the instruction's B-negate bit)
+//   Di += Xr Wi^T + Xi Wr^T
+// M = 128 rows (tiles x batch), N = fo output maps, K = input maps in chunks
+// of 8 (one tf32 MMA K-step).  Spectra use 128-byte lines of 16 frequencies
+// ([w/16][row][channel][w%16]); a CTA tile is one frequency PAIR (a 16-byte
+// piece of each line) x 128 rows, so 4 accumulators of N columns = 4*fo <= 512
+// TMEM columns.  Tiles are ordered (line block, m-block, pair) with the pair
+// fastest: the 8 CTAs reading pieces of the same lines run concurrently and
+// share them through L2.
+//
+// Persistent, warp-specialised pipeline over a flat stream of (tile, K-chunk)
+// items and a 3-slot shared-memory ring (raw X chunk | pre-split W chunk |
+// split X chunk per slot), handshakes on mbarriers:
+//   warp 0        producer: cp.async of the raw X chunk (rows padded to
+//                 144 B) + one bulk copy of the W chunk (already tf32 hi/lo in
+//                 the UMMA layout, written once per layer by wsplit_kernel);
+//                 completion tracked on full[slot];
+//   warps 8-11    converters: split X into tf32 hi/lo in the canonical
+//                 K-major no-swizzle core-matrix layout, fence the async
+//                 proxy, arrive on ready[slot];
+//   warp 1        MMA issuer (one thread): 24 tcgen05.mma per chunk, commit to
+//                 empty[slot] (frees the slot) and, after a tile's last chunk,
+//                 to tmem_full;
+//   warps 4-7     epilogue (TMEM lane quadrants 0-3): tcgen05.ld, 16-byte
+//                 stores of the Y pieces, arrive on tmem_empty.
+#include "async.cuh"
+#include "common.cuh"
+#include "fftconv.hpp"
+
+namespace vxg {
+namespace {
+
+constexpr int TC_M = 128;
+constexpr int TC_KC = 8;
+constexpr int TC_SLOTS = 3;
+constexpr int TC_THREADS = 384;  // 12 warps
+constexpr int RAW_ROW = 144;     // padded raw-row stride (bytes)
+
+template <int FO>
+struct TcCfg {
+  static constexpr int A_MAT = TC_M * TC_KC * 4;   // one 128 x 8 tf32 matrix
+  static constexpr int B_MAT = FO * TC_KC * 4;     // one FO x 8 tf32 matrix
+  static constexpr int B_CHUNK = 8 * B_MAT;        // pre-split W chunk (w, re/im, hi/lo)
+  static constexpr int RAW_A = TC_M * RAW_ROW;
+  static constexpr int OFF_W = RAW_A;
+  static constexpr int OFF_A = RAW_A + B_CHUNK;    // split X (8 matrices)
+  static constexpr int SLOT = OFF_A + 8 * A_MAT;
+  static constexpr int SMEM = TC_SLOTS * SLOT + 128;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// K-major, no swizzle: core matrix = 8 rows x 16 B contiguous; LBO = 128 B
+// between the two K halves, SBO = 256 B between 8-row groups; version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
+         (uint64_t(1) << 46);
+}
+
+// byte offset of (row, k-group of 4) in a K-major 8-wide tile
+__host__ __device__ __forceinline__ int tile_off(int row, int kgroup) {
+  return (row >> 3) * 256 + kgroup * 128 + (row & 7) * 16;
+}
+
+__device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // exactly representable in tf32
+  lo = v - hi;                                             // exact in fp32
+}
+
+template <int N>
+__device__ __forceinline__ constexpr uint32_t idesc_tf32(bool neg_b) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(neg_b) << 14) | (uint32_t(N >> 3) << 17) |
+         (uint32_t(TC_M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;\n" ::"r"(bytes),
+               "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// ---- one-time W preparation: raw [w/16][i][j][16] complex -> per (pair, chunk)
+// the 8 matrices (w, re/im, hi/lo) of FO x 8 tf32 in the UMMA layout.
+template <int FO>
+__global__ void wsplit_kernel(const float4* __restrict__ raw, uint8_t* __restrict__ out,
+                              int64_t npairs, int f) {
+  using C = TcCfg<FO>;
+  const int nchunks = f / TC_KC;
+  const int64_t total = npairs * nchunks * FO * 2;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int hk = int(t & 1);
+    const int i = int((t >> 1) % FO);
+    const int64_t pc = (t >> 1) / FO;  // pair * nchunks + kc
+    const int kc = int(pc % nchunks);
+    const int64_t pair = pc / nchunks;
+    const int64_t wb = pair >> 3;
+    const int pip = int(pair & 7);
+    const float4* src = raw + ((wb * FO + i) * f + kc * TC_KC + 4 * hk) * 8 + pip;
+    float4 v[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) v[kk] = src[kk * 8];
+    uint8_t* dst = out + pc * C::B_CHUNK;
+#pragma unroll
+    for (int wc = 0; wc < 4; ++wc) {
+      float h[4], l[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float x = wc == 0 ? v[kk].x : wc == 1 ? v[kk].y : wc == 2 ? v[kk].z : v[kk].w;
+        split_tf32(x, h[kk], l[kk]);
+      }
+      *reinterpret_cast<float4*>(dst + (wc * 2 + 0) * C::B_MAT + tile_off(i, hk)) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(dst + (wc * 2 + 1) * C::B_MAT + tile_off(i, hk)) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+  }
+}
+
+struct TileCoord {
+  int64_t wb, m0, pair;
+  int pip;
+};
+
+template <int FO>
+__global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
+  using C = TcCfg<FO>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_SLOTS * C::SLOT);
+  uint64_t* ready = full + TC_SLOTS;
+  uint64_t* empty = ready + TC_SLOTS;
+  uint64_t* tmem_full = empty + TC_SLOTS;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nchunks = a.f / TC_KC;
+  const int64_t ntiles = int64_t(a.mblocks) * a.npairs;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nitems = my_tiles * nchunks;
+
+  auto coord = [&](int64_t local_tile) {
+    const int64_t tile = blockIdx.x + local_tile * gridDim.x;
+    TileCoord tc;
+    tc.pip = int(tile & 7);
+    const int64_t rest = tile >> 3;
+    tc.m0 = (rest % a.mblocks) * TC_M;
+    tc.wb = rest / a.mblocks;
+    tc.pair = tc.wb * 8 + tc.pip;
+    return tc;
+  };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 32) {
+    for (int s = 0; s < TC_SLOTS; ++s) {
+      mbar_init(&full[s], 32 + 1);  // 32 producer lanes (cp.async) + the W bulk copy arrive
+      mbar_init(&ready[s], 128);    // converter threads
+      mbar_init(&empty[s], 1);      // MMA commit
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 128);     // epilogue threads
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    const float4* xsrc = reinterpret_cast<const float4*>(a.X);  // one float4 = 2 complex
+    for (int64_t g = 0; g < nitems; ++g) {
+      const int s = int(g % TC_SLOTS);
+      if (g >= TC_SLOTS) mbar_wait(&empty[s], uint32_t((g / TC_SLOTS - 1) & 1));
+      const TileCoord tc = coord(g / nchunks);
+      const int kc = int(g % nchunks);
+      uint8_t* slot = smem + s * C::SLOT;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], C::B_CHUNK);
+        bulk_copy(slot + C::OFF_W,
+                  reinterpret_cast<const uint8_t*>(a.W) + (tc.pair * nchunks + kc) * int64_t(C::B_CHUNK),
+                  C::B_CHUNK, &full[s]);
+      }
+#pragma unroll 4
+      for (int u = lane; u < TC_M * TC_KC; u += 32) {
+        const int row = u >> 3, jj = u & 7;
+        const bool ok = tc.m0 + row < a.M;
+        const float4* src =
+            ok ? xsrc + ((tc.wb * a.mstride + tc.m0 + row) * a.f + kc * TC_KC + jj) * 8 + tc.pip : xsrc;
+        cp_async16(slot + row * RAW_ROW + jj * 16, src, ok);
+      }
+      cp_async_arrive_noinc(&full[s]);
+    }
+  } else if (warp >= 8) {
+    // ---------------- converters: thread c owns row c ----------------
+    const int c = tid - 256;
+    for (int64_t g = 0; g < nitems; ++g) {
+      const int s = int(g % TC_SLOTS);
+      mbar_wait(&full[s], uint32_t((g / TC_SLOTS) & 1));
+      uint8_t* slot = smem + s * C::SLOT;
+      const uint8_t* raw = slot + c * RAW_ROW;
+#pragma unroll
+      for (int hk = 0; hk < 2; ++hk) {
+        float4 v[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) v[kk] = *reinterpret_cast<const float4*>(raw + (4 * hk + kk) * 16);
+#pragma unroll
+        for (int wc = 0; wc < 4; ++wc) {
+          float h[4], l[4];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const float x = wc == 0 ? v[kk].x : wc == 1 ? v[kk].y : wc == 2 ? v[kk].z : v[kk].w;
+            split_tf32(x, h[kk], l[kk]);
+          }
+          *reinterpret_cast<float4*>(slot + C::OFF_A + (wc * 2 + 0) * C::A_MAT + tile_off(c, hk)) =
+              make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(slot + C::OFF_A + (wc * 2 + 1) * C::A_MAT + tile_off(c, hk)) =
+              make_float4(l[0], l[1], l[2], l[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);  // generic-proxy STS -> tensor core
+      mbar_arrive(&ready[s]);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      for (int64_t g = 0; g < nitems; ++g) {
+        const int s = int(g % TC_SLOTS);
+        const int kc = int(g % nchunks);
+        const int64_t t = g / nchunks;
+        if (kc == 0 && t > 0) mbar_wait(tmem_empty, uint32_t((t - 1) & 1));  // epilogue drained TMEM
+        mbar_wait(&ready[s], uint32_t((g / TC_SLOTS) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const uint32_t slot = smem_u32(smem + s * C::SLOT);
+        const uint32_t sa = slot + C::OFF_A, sb = slot + C::OFF_W;
+        const uint32_t first = kc > 0 ? 1u : 0u;
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const uint32_t dr = tmem + w * 2 * FO, di = dr + FO;
+          auto am = [&](int cc, int h) { return umma_desc(sa + ((w * 2 + cc) * 2 + h) * C::A_MAT); };
+          auto bm = [&](int cc, int h) { return umma_desc(sb + ((w * 2 + cc) * 2 + h) * C::B_MAT); };
+          mma_tf32(dr, am(0, 0), bm(0, 0), idesc_tf32<FO>(false), first);  // Dr += Xr Wr
+          mma_tf32(dr, am(0, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32(dr, am(0, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
+          mma_tf32(dr, am(1, 0), bm(1, 0), idesc_tf32<FO>(true), 1);       // Dr -= Xi Wi
+          mma_tf32(dr, am(1, 0), bm(1, 1), idesc_tf32<FO>(true), 1);
+          mma_tf32(dr, am(1, 1), bm(1, 0), idesc_tf32<FO>(true), 1);
+          mma_tf32(di, am(0, 0), bm(1, 0), idesc_tf32<FO>(false), first);  // Di += Xr Wi
+          mma_tf32(di, am(0, 0), bm(1, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32(di, am(0, 1), bm(1, 0), idesc_tf32<FO>(false), 1);
+          mma_tf32(di, am(1, 0), bm(0, 0), idesc_tf32<FO>(false), 1);      // Di += Xi Wr
+          mma_tf32(di, am(1, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32(di, am(1, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
+        }
+        umma_commit(&empty[s]);                       // slot reusable once these MMAs finish
+        if (kc == nchunks - 1) umma_commit(tmem_full);  // tile accumulated
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp 4+q owns TMEM lanes 32q .. 32q+31 ----------------
+    const int q = warp - 4;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      mbar_wait(tmem_full, uint32_t(t & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const TileCoord tc = coord(t);
+      const int64_t m = tc.m0 + row;
+      float4* yrow = reinterpret_cast<float4*>(a.Y) + (tc.wb * a.mstride + m) * a.fo * 8 + tc.pip;
+#pragma unroll 1
+      for (int i0 = 0; i0 < FO; i0 += 16) {
+        uint32_t v[4][16];  // (w0 re, w0 im, w1 re, w1 im) x 16 maps
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const uint32_t col = (qq >> 1) * 2 * FO + (qq & 1) * FO + i0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+              "[%16];\n"
+              : "=r"(v[qq][0]), "=r"(v[qq][1]), "=r"(v[qq][2]), "=r"(v[qq][3]), "=r"(v[qq][4]),
+                "=r"(v[qq][5]), "=r"(v[qq][6]), "=r"(v[qq][7]), "=r"(v[qq][8]), "=r"(v[qq][9]),
+                "=r"(v[qq][10]), "=r"(v[qq][11]), "=r"(v[qq][12]), "=r"(v[qq][13]), "=r"(v[qq][14]),
+                "=r"(v[qq][15])
+              : "r"(lane_base + col));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        if (m < a.M) {
+#pragma unroll
+          for (int ii = 0; ii < 16; ++ii)
+            yrow[(i0 + ii) * 8] = make_float4(__uint_as_float(v[0][ii]), __uint_as_float(v[1][ii]),
+                                              __uint_as_float(v[2][ii]), __uint_as_float(v[3][ii]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(tmem_empty);
+    }
+  }
+  // warps 2-3 have no role
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int FO>
+void tc_t(Ctx* c, GemmArgs a) {
+  using C = TcCfg<FO>;
+  static bool configured = false;
+  if (!configured) {
+    VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_tc_kernel<FO>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  a.mblocks = int((a.M + TC_M - 1) / TC_M);
+  const int64_t ntiles = int64_t(a.mblocks) * a.npairs;  // npairs = 8 per 16-frequency line
+  const unsigned grid = unsigned(std::min<int64_t>(ntiles, c->num_sms));
+  cgemm_tc_kernel<FO><<<grid, TC_THREADS, C::SMEM, c->stream>>>(a);
+  c->counted();
+  check_launch("cgemm_tc_kernel");
+}
+
+template <int FO>
+void wsplit_t(Ctx* c, const float2* raw, void* out, int64_t npairs, int f) {
+  const int64_t total = npairs * (f / TC_KC) * FO * 2;
+  wsplit_kernel<FO><<<grid_for(total, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
+      reinterpret_cast<const float4*>(raw), static_cast<uint8_t*>(out), npairs, f);
+  c->counted();
+  check_launch("wsplit_kernel");
+}
+
+}  // namespace
+
+// fo <= 80 keeps the 3-slot ring (raw X | split W | split X) inside 227 KB of smem
+bool cgemm_tc_supported(int64_t f, int64_t fo) {
+  return f % TC_KC == 0 && f >= TC_KC && fo % 16 == 0 && fo >= 16 && fo <= 80;
+}
+
+int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
+  return npairs * (f / TC_KC) * 8 * fo * TC_KC * 4;
+}
+
+#define VXG_TC_SWITCH(CALL)                                           \
+  switch (fo) {                                                       \
+    case 16: CALL(16); break;                                         \
+    case 32: CALL(32); break;                                         \
+    case 48: CALL(48); break;                                         \
+    case 64: CALL(64); break;                                         \
+    case 80: CALL(80); break;                                         \
+    default: throw invalid("cgemm_tc: unsupported output map count"); \
+  }
+
+void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo) {
+  KScope ks(c, VXG_K_KSPEC, 0.0, double(npairs) * f * fo * (16.0 + 32.0));
+#define VXG_WS(F) wsplit_t<F>(c, raw, out, npairs, int(f))
+  VXG_TC_SWITCH(VXG_WS)
+#undef VXG_WS
+}
+
+// Y[w/16][row][fo][16] = X[w/16][row][f][16] . W (pre-split by tc_wsplit)
+void launch_cgemm_tc(Ctx* c, const GemmArgs& a, int64_t npairs) {
+  const double nw = double(a.T) * a.T * (a.T / 2 + 1);
+  KScope ks(c, VXG_K_CGEMM, 8.0 * double(a.M) * a.f * a.fo * nw,
+            8.0 * nw * (double(a.M) * a.f + double(a.M) * a.fo + double(a.f) * a.fo));
+  GemmArgs b = a;
+  b.npairs = npairs;
+  const int64_t fo = a.fo;
+#define VXG_TC(F) tc_t<F>(c, b)
+  VXG_TC_SWITCH(VXG_TC)
+#undef VXG_TC
+}
+
+}  // namespace vxg

@@ -53,7 +53,6 @@ struct TileCfg {
   static constexpr int PADX = ((H - (T * SY) % 16) % 16 + 16) % 16;
   static constexpr int SX = T * SY + PADX;                  // x-plane stride
   static constexpr int NW = T * T * H;                      // frequencies per tile
-  static constexpr int NWB = (NW + WB - 1) / WB;
   static constexpr int SMEM = T * SX * 8;                   // bytes
   static constexpr int THREADS = ((T * H + 31) / 32) * 32;  // one line per thread per pass
   static constexpr int MINB = T >= 28 ? 1 : (T >= 24 ? 2 : (T >= 20 ? 3 : 4));
@@ -78,15 +77,27 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const float* img = a.src + (s * a.f + j) * a.img_stride;
   const int tid = threadIdx.x;
 
-  // A0: real box -> slots (asynchronous 4-byte copies, zero outside the image)
+  // A0: real box -> slots (asynchronous 4-byte copies, zero outside the image).
+  // Warp w owns x planes w, w + nwarps, ...; lane = z; rows advance by
+  // pointer increments (no per-element index arithmetic).
+  {
+    constexpr int NWARPS = C::THREADS / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gz = oz + lane;
+    const bool zin = lane < T && gz < a.nz;
+    for (int x = warp; x < T; x += NWARPS) {
+      const int gx = ox + x;
+      const bool xin = zin && gx < a.nx;
+      const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
+      float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 4
-  for (int idx = tid; idx < T * T * T; idx += C::THREADS) {
-    const int z = idx % T, l = idx / T;
-    const int y = l % T, x = l / T;
-    const int gx = ox + x, gy = oy + y, gz = oz + z;
-    const bool in = gx < a.nx && gy < a.ny && gz < a.nz;
-    const float* g = in ? img + (int64_t(gx) * a.ny + gy) * a.nz + gz : img;
-    cp_async4(spf + 2 * (x * C::SX + y * C::SY) + z, g, in);
+      for (int y = 0; y < T; ++y) {
+        const bool in = xin && oy + y < a.ny;
+        if (lane < T) cp_async4(d, in ? g : img, in);
+        g += a.nz;
+        d += 2 * C::SY;
+      }
+    }
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -143,16 +154,25 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   }
   __syncthreads();
 
-  // D: spectrum lines, zero tail up to NWB*16
-  float2* dst = a.out + (ml * a.f + j) * WB;
-  const int64_t wb_stride = a.mstride * a.f * WB;
-  for (int w = tid; w < C::NWB * WB; w += C::THREADS) {
-    float2 v = make_float2(0.f, 0.f);
-    if (w < C::NW) {
-      const int kx = w / (T * C::H), r = w % (T * C::H);
-      v = sp[C::idx(kx, r / C::H, r % C::H)];
+  // D: spectrum chunks of lw frequencies (lw a power of two).  Thread t <
+  // T*H owns (ky, kz) = (t / H, t % H) and walks kx: w = kx*T*H + t.
+  const int lw = a.lw, lshift = __ffs(lw) - 1;
+  float2* dst = a.out + (ml * a.f + j) * lw;
+  const int64_t wb_stride = a.mstride * a.f * lw;
+  if (tid < T * C::H) {
+    const float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
+    int w = tid;
+#pragma unroll 4
+    for (int kx = 0; kx < T; ++kx) {
+      dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = s[kx * C::SX];
+      w += T * C::H;
     }
-    dst[(w / WB) * wb_stride + (w % WB)] = v;
+  }
+  // zero tail up to a multiple of lw (read by the FFMA contraction only)
+  const int nwp = ((C::NW + lw - 1) / lw) * lw;
+  if (tid < nwp - C::NW) {
+    const int w = C::NW + tid;
+    dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = make_float2(0.f, 0.f);
   }
 }
 
@@ -173,12 +193,17 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const int tid = threadIdx.x;
 
   // A: spectrum lines -> smem (asynchronous 8-byte copies)
-  const float2* src = a.spec + (ml * a.fo + i) * WB;
-  const int64_t wb_stride = a.mstride * a.fo * WB;
+  const int lw = a.lw, lshift = __ffs(lw) - 1;
+  const float2* src = a.spec + (ml * a.fo + i) * lw;
+  const int64_t wb_stride = a.mstride * a.fo * lw;
+  if (tid < T * C::H) {
+    float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
+    int w = tid;
 #pragma unroll 4
-  for (int w = tid; w < C::NW; w += C::THREADS) {
-    const int kx = w / (T * C::H), r = w % (T * C::H);
-    cp_async8(sp + C::idx(kx, r / C::H, r % C::H), src + (w / WB) * wb_stride + (w % WB));
+    for (int kx = 0; kx < T; ++kx) {
+      cp_async8(s + kx * C::SX, src + int64_t(w >> lshift) * wb_stride + (w & (lw - 1)));
+      w += T * C::H;
+    }
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -249,17 +274,26 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   }
   __syncthreads();
 
-  // E: coalesced store of the crop, clipped to the output image
-  float* out = a.dst + (s * a.fo + i) * a.oel;
-  const int gx0 = tx * a.vx, gy0 = ty * a.vy, gz0 = tz * a.vz;
-  const int V = a.vx * a.vy * a.vz;
-  for (int idx = tid; idx < V; idx += C::THREADS) {
-    const int z = idx % a.vz, l = idx / a.vz;
-    const int y = l % a.vy, x = l / a.vy;
-    const int gx = gx0 + x, gy = gy0 + y, gz = gz0 + z;
-    if (gx < a.onx && gy < a.ony && gz < a.onz)
-      out[(int64_t(gx) * a.ony + gy) * a.onz + gz] =
-          spf[2 * ((a.cx + x) * C::SX + (a.cy + y) * C::SY) + a.cz + z];
+  // E: store of the crop, clipped to the output image: warp w owns x planes
+  // w, w + nwarps, ...; lane = z; rows advance by pointer increments.
+  {
+    constexpr int NWARPS = C::THREADS / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gx0 = tx * a.vx, gy0 = ty * a.vy, gz = tz * a.vz + lane;
+    const bool zin = lane < a.vz && gz < a.onz;
+    const int ylim = min(a.vy, a.ony - gy0);
+    for (int x = warp; x < a.vx; x += NWARPS) {
+      const int gx = gx0 + x;
+      if (!zin || gx >= a.onx) continue;
+      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.onz + gz;
+      const float* r = spf + 2 * ((a.cx + x) * C::SX + a.cy * C::SY) + a.cz + lane;
+#pragma unroll 4
+      for (int y = 0; y < ylim; ++y) {
+        *o = *r;
+        o += a.onz;
+        r += 2 * C::SY;
+      }
+    }
   }
 }
 
@@ -297,7 +331,10 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
 const int kTileSizes[] = {4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32};
 const int kNumTileSizes = sizeof(kTileSizes) / sizeof(int);
 
-int64_t tile_nwb(int T) { return (int64_t(T) * T * (T / 2 + 1) + WB - 1) / WB; }
+int64_t tile_nwp(int T, int lw) {
+  const int64_t nw = int64_t(T) * T * (T / 2 + 1);
+  return ((nw + lw - 1) / lw) * lw;
+}
 
 #define VXG_TILE_SWITCH(FN)                                         \
   switch (T) {                                                      \
