@@ -11,6 +11,9 @@
 // `if (v > m) m = v` starting from the first element, so ties between +0 and
 // -0 resolve to the same element.  NaN inputs set the context flag, which the
 // host turns into VXG_INVALID like check_no_nan (layers.hpp:111-116).
+#include <algorithm>
+
+#include "async.cuh"
 #include "common.cuh"
 
 namespace vxg {
@@ -199,6 +202,92 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
   if (saw_nan) *nan_flag = 1;
 }
 
+// p = 2 MPF, HBM-rate version: the CTA stages its input box
+// (XT+1) x (TY+1) x (TZ+1) in shared memory with coalesced cp.async (every
+// input element crosses the load path once), then each thread walks x down
+// one (y, z) column computing the 2x2 row maxima and the 2-row D values from
+// shared memory, writing each D value to its fragment.  Same scan order and
+// update rule as the reference (first of equal elements wins).
+// Each thread owns two adjacent z columns so a warp writes 32 consecutive
+// floats (a full 128-byte line) into each of the two z-parity fragments.
+constexpr int M2_TZ = 64, M2_TY = 8, M2_XT = 16;
+constexpr int M2_BZ = M2_TZ + 2, M2_BY = M2_TY + 1, M2_BX = M2_XT + 1;  // row padded to even
+
+__global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ in,
+                                                     float* __restrict__ out, MpfGeom g,
+                                                     int* __restrict__ nan_flag) {
+  __shared__ __align__(16) float box[M2_BX * M2_BY * M2_BZ];
+  const int tile = blockIdx.x;
+  const int tz = tile % g.tiles_z, ty = (tile / g.tiles_z) % g.tiles_y, tx = tile / (g.tiles_z * g.tiles_y);
+  const int z0 = tz * M2_TZ, y0 = ty * M2_TY, x0 = tx * M2_XT;
+  const int lz = threadIdx.x % 32, ly = threadIdx.x / 32;
+  const int z = z0 + 2 * lz, y = y0 + ly;  // columns z (even) and z + 1
+  const int x1 = min(M2_XT, g.dx - x0);
+  const bool live = z < g.dz && y < g.dy;    // dz is even: z + 1 < dz too
+  const int64_t nel = int64_t(g.nx) * g.ny * g.nz;
+  const int moel = g.mx * g.my * g.mz;
+  const int64_t fstride = int64_t(g.f_tot) * moel;
+  const int offy = (y & 1) * 2;
+  bool saw_nan = false;
+  for (int64_t plane = blockIdx.y; plane < g.planes; plane += gridDim.y) {
+    const float* src = in + plane * nel;
+    __syncthreads();  // previous plane's readers are done with the box
+    {
+      // warp per box row, lane = z (coalesced 4-byte copies)
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      for (int r = w; r < M2_BX * M2_BY; r += 8) {
+        const int bx = r / M2_BY, by = r % M2_BY;
+        const int gx = x0 + bx, gy = y0 + by;
+        const bool rok = gx < g.nx && gy < g.ny;
+        const float* row = src + (int64_t(gx) * g.ny + gy) * g.nz + z0;
+#pragma unroll
+        for (int bz = lane; bz < M2_BZ; bz += 32) {
+          const bool ok = rok && z0 + bz < g.nz;
+          cp_async4(&box[r * M2_BZ + bz], ok ? row + bz : src, ok);
+        }
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (!live) continue;
+    const int64_t s = plane / g.f;
+    const int fm = int(plane % g.f);
+    float* dst0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.mz + (z >> 1);
+    const float* col = box + ly * M2_BZ + 2 * lz;
+    float prev0 = 0.f, prev1 = 0.f;
+#pragma unroll 4
+    for (int xr = 0; xr <= x1; ++xr) {
+      const float* rw = col + xr * (M2_BY * M2_BZ);
+      const float2 a01 = *reinterpret_cast<const float2*>(rw);
+      const float2 b01 = *reinterpret_cast<const float2*>(rw + M2_BZ);
+      const float a2 = rw[2], b2 = rw[M2_BZ + 2];
+      saw_nan |= (a01.x != a01.x) | (a01.y != a01.y) | (a2 != a2) | (b01.x != b01.x) |
+                 (b01.y != b01.y) | (b2 != b2);
+      // column z: (y, z), (y, z+1), (y+1, z), (y+1, z+1) in scan order
+      float m0 = a01.x;
+      m0 = a01.y > m0 ? a01.y : m0;
+      m0 = b01.x > m0 ? b01.x : m0;
+      m0 = b01.y > m0 ? b01.y : m0;
+      // column z+1
+      float m1 = a01.y;
+      m1 = a2 > m1 ? a2 : m1;
+      m1 = b01.y > m1 ? b01.y : m1;
+      m1 = b2 > m1 ? b2 : m1;
+      if (xr > 0) {
+        const int xd = x0 + xr - 1;
+        const int64_t o = int64_t(xd >> 1) * g.my * g.mz;
+        const int ox = (xd & 1) * 4 + offy;
+        dst0[(ox + 0) * fstride + o] = m0 > prev0 ? m0 : prev0;
+        dst0[(ox + 1) * fstride + o] = m1 > prev1 ? m1 : prev1;
+      }
+      prev0 = m0;
+      prev1 = m1;
+    }
+  }
+  if (saw_nan) *nan_flag = 1;
+}
+
 __global__ void nan_check_kernel(const float* __restrict__ x, int64_t n, int* flag) {
   bool bad = false;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -272,9 +361,15 @@ void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i
   dim3 grid(unsigned(tiles), unsigned(std::min<int64_t>(g.planes, 65535)));
   KScope ks(c, VXG_K_POOL, 0.0,
             4.0 * double(g.planes) * (double(n.x) * n.y * n.z + double(g.P) * g.mx * g.my * g.mz));
-  if (g.px == 2 && g.py == 2 && g.pz == 2)
-    mpf_full_kernel<2, 2, 2><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
-  else
+  if (g.px == 2 && g.py == 2 && g.pz == 2) {
+    MpfGeom h = g;
+    h.tiles_z = (g.dz + M2_TZ - 1) / M2_TZ;
+    h.tiles_y = (g.dy + M2_TY - 1) / M2_TY;
+    h.tiles_x = (g.dx + M2_XT - 1) / M2_XT;
+    const int64_t t2 = int64_t(h.tiles_z) * h.tiles_y * h.tiles_x;
+    dim3 grid2(unsigned(t2), unsigned(std::min<int64_t>(g.planes, 65535)));
+    mpf222_kernel<<<grid2, 256, 0, c->stream>>>(in, out, h, c->d_flag);
+  } else
     mpf_full_kernel<0, 0, 0><<<grid, 256, 0, c->stream>>>(in, out, g, c->d_flag);
   c->counted();
   check_launch("mpf_full_kernel");
