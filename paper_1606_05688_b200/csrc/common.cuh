@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
 #include <cstdint>
 #include <mutex>
 #include <stdexcept>
@@ -31,6 +32,9 @@ struct cuda_failure : std::runtime_error {
 struct parse_failure : std::runtime_error {
   explicit parse_failure(const std::string& w) : std::runtime_error(w) {}
 };
+
+// VXG_TRACE=1: the executor and layer drivers print their plans to stderr
+bool trace_on();
 
 inline void require(bool cond, const char* what) {
   if (!cond) throw invalid(what);
@@ -62,6 +66,60 @@ struct KRecord {
   double flops, bytes;
 };
 
+// Best-fit sub-allocator over one device block (coalescing free list).  All
+// work runs on the context's single stream, so a block freed on the host may
+// be handed out again at once: the next user is stream-ordered after the last.
+struct Arena {
+  char* base = nullptr;
+  i64 size = 0;
+  std::map<i64, i64> free_;  // offset -> bytes
+
+  static constexpr i64 kAlign = 512;
+  void reset(void* b, i64 n) {
+    base = static_cast<char*>(b);
+    size = n;
+    free_.clear();
+    if (n > 0) free_[0] = n;
+  }
+  void* alloc(i64 bytes) {
+    bytes = (bytes + kAlign - 1) / kAlign * kAlign;
+    auto best = free_.end();
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= bytes && (best == free_.end() || it->second < best->second)) best = it;
+    if (best == free_.end()) return nullptr;
+    const i64 off = best->first, len = best->second;
+    free_.erase(best);
+    if (len > bytes) free_[off + bytes] = len - bytes;
+    return base + off;
+  }
+  void release(void* p, i64 bytes) {
+    bytes = (bytes + kAlign - 1) / kAlign * kAlign;
+    i64 off = static_cast<char*>(p) - base;
+    auto next = free_.lower_bound(off);
+    if (next != free_.end() && next->first == off + bytes) {
+      bytes += next->second;
+      next = free_.erase(next);
+    }
+    if (next != free_.begin()) {
+      auto prev = std::prev(next);
+      if (prev->first + prev->second == off) {
+        prev->second += bytes;
+        return;
+      }
+    }
+    free_[off] = bytes;
+  }
+  bool owns(const void* p) const {
+    const char* q = static_cast<const char*>(p);
+    return base && q >= base && q < base + size;
+  }
+  i64 largest() const {
+    i64 m = 0;
+    for (const auto& kv : free_) m = std::max(m, kv.second);
+    return m;
+  }
+};
+
 // One context per GPU.  All work is issued on `stream`; allocations are
 // stream-ordered (cudaMallocAsync) and charged against `budget` bytes.
 struct Ctx {
@@ -78,6 +136,13 @@ struct Ctx {
   bool prof = false;
   std::vector<KRecord> krec;
   std::vector<cudaEvent_t> spare_events;
+  Arena* arena = nullptr;  // set while a network forward runs (forward.cu)
+
+  // bytes a new allocation can get: the largest arena block, else the budget left
+  i64 avail() {
+    std::lock_guard<std::mutex> lk(mu);
+    return arena ? arena->largest() : budget - current;
+  }
 
   cudaEvent_t take_event() {
     if (!spare_events.empty()) {
@@ -134,21 +199,42 @@ class DevBuf {
   ~DevBuf() { reset(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : c_(o.c_), p_(o.p_), n_(o.n_) { o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0; }
+  DevBuf(DevBuf&& o) noexcept : c_(o.c_), p_(o.p_), n_(o.n_), arena_(o.arena_) {
+    o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0; o.arena_ = nullptr;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       reset();
-      c_ = o.c_; p_ = o.p_; n_ = o.n_;
-      o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0;
+      c_ = o.c_; p_ = o.p_; n_ = o.n_; arena_ = o.arena_;
+      o.c_ = nullptr; o.p_ = nullptr; o.n_ = 0; o.arena_ = nullptr;
     }
     return *this;
   }
   void alloc(Ctx* c, i64 bytes) {
     reset();
     if (bytes <= 0) return;
+    if (c->arena) {
+      void* q = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(c->mu);
+        q = c->arena->alloc(bytes);
+      }
+      if (q) {
+        c_ = c; p_ = q; n_ = bytes; arena_ = c->arena;
+        return;
+      }
+    }
     c->charge(bytes);
     void* p = nullptr;
     cudaError_t e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
+    if (e == cudaErrorMemoryAllocation) {
+      // the pool keeps freed blocks mapped (release threshold = max); when none
+      // of them fits, hand them back and map the request afresh
+      cudaGetLastError();
+      cudaStreamSynchronize(c->stream);
+      cudaMemPoolTrimTo(c->pool, 0);
+      e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
+    }
     if (e != cudaSuccess) {
       c->release(bytes);
       cudaGetLastError();
@@ -159,11 +245,14 @@ class DevBuf {
     c_ = c; p_ = p; n_ = bytes;
   }
   void reset() {
-    if (p_) {
+    if (p_ && arena_) {
+      std::lock_guard<std::mutex> lk(c_->mu);
+      arena_->release(p_, n_);
+    } else if (p_) {
       cudaFreeAsync(p_, c_->stream);
       c_->release(n_);
     }
-    c_ = nullptr; p_ = nullptr; n_ = 0;
+    c_ = nullptr; p_ = nullptr; n_ = 0; arena_ = nullptr;
   }
   template <class T = float>
   T* as() const { return static_cast<T*>(p_); }
@@ -174,6 +263,7 @@ class DevBuf {
   Ctx* c_ = nullptr;
   void* p_ = nullptr;
   i64 n_ = 0;
+  Arena* arena_ = nullptr;
 };
 
 inline unsigned grid_for(i64 n, int block, i64 cap = (i64(1) << 31) - 1) {

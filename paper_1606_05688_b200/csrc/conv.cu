@@ -4,6 +4,7 @@
 // reference's transform scratch (proj/include/voxin/fft.hpp:74-90).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -22,8 +23,25 @@ bool tc_disabled() {
 
 }  // namespace
 
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("VXG_TRACE");
+    return e && std::strcmp(e, "0") != 0;
+  }();
+  return on;
+}
+
+int64_t fft_reserved_rows() {
+  static const int64_t r = [] {
+    const char* e = std::getenv("VXG_FFT_ROWS");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? int64_t(v) : int64_t(256);
+  }();
+  return r;
+}
+
 int64_t fft_chunk_bytes(const FftPlan& plan, int64_t f, int64_t fo, int64_t rows) {
-  return rows * (f + fo) * plan.nwp * 8;
+  return rows * (plan.inplace ? f : f + fo) * plan.nwp * 8;
 }
 
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
@@ -51,6 +69,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tiles = p.nt.vol();
     p.lw = 16;
     p.tc = tc;
+    p.inplace = tc && f == fo;
     p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);
     const double nw = double(T) * T * (T / 2 + 1);
@@ -115,15 +134,18 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
   const int64_t M = S * plan.tiles;
   const int64_t per_row = fft_chunk_bytes(plan, f, fo, 1);
   int64_t avail = spectra_budget;
-  if (avail <= 0) {
-    std::lock_guard<std::mutex> lk(c->mu);
-    avail = int64_t(double(c->budget - c->current) * 0.95);
-  }
+  if (avail <= 0) avail = int64_t(double(c->avail()) * 0.98);
   int64_t rows = std::max<int64_t>(1, avail / per_row);
   rows = std::min(rows, M);
   rows = std::min<int64_t>(rows, ((int64_t(1) << 31) - 1) / std::max(f, fo));
+  if (trace_on())
+    std::fprintf(stderr, "[vxg] conv_fft S=%lld f=%lld fo=%lld n=%lld T=%d tiles=%lld M=%lld rows=%lld tc=%d\n",
+                 (long long)S, (long long)f, (long long)fo, (long long)n.x, T, (long long)plan.tiles,
+                 (long long)M, (long long)rows, int(plan.tc));
   DevBuf X(c, rows * f * plan.nwp * 8);
-  DevBuf Y(c, rows * fo * plan.nwp * 8);
+  DevBuf Ybuf;
+  if (!plan.inplace) Ybuf.alloc(c, rows * fo * plan.nwp * 8);
+  const DevBuf& Y = plan.inplace ? X : Ybuf;
 
   for (int64_t m0 = 0; m0 < M; m0 += rows) {
     const int64_t mc = std::min(rows, M - m0);

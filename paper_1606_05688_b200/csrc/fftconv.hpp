@@ -76,6 +76,8 @@ struct FftPlan {
   int64_t tiles = 0;
   int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
+  bool inplace = false;  // tc with f == fo: Y overwrites X (each CTA tile reads
+                         // exactly the bytes it later writes, see k_cgemm_tc.cu)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };
@@ -96,6 +98,9 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
 void conv_direct_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
                         int64_t fo, V3 k, const float* bias, bool relu, float* out);
 
+// rows of spectrum chunk the executor reserves per FFT layer (the chunk grows
+// into whatever the budget leaves; VXG_FFT_ROWS overrides)
+int64_t fft_reserved_rows();
 // peak scratch bytes conv_fft_device needs beyond in/out (one chunk of rows)
 int64_t fft_chunk_bytes(const FftPlan& plan, int64_t f, int64_t fo, int64_t rows);
 

@@ -12,7 +12,10 @@
 // batch order (s * P + offset at every pool), so the leaves write the final
 // fragment tensor in exactly the order recombine_fragments expects.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <map>
+#include <tuple>
 
 #include "forward.hpp"
 
@@ -113,28 +116,40 @@ struct Step {
   int64_t P;  // entries produced per input entry
 };
 
-// Memory model of the executor.  need_min[li] is the peak (bytes, input of
-// layer li excluded) of running layers [li, L) on ONE entry with groups of one
-// entry everywhere below -- independent of the batch, so the greedy group
-// choice at each level is a single binary search.
+// Memory model of the executor.  A schedule is fixed by a target row count R
+// for the FFT layers: a layer's useful group ("want") is the number of
+// entries that gives its per-frequency contraction R rows (FFT conv) or that
+// feeds the next layer's want (everything else), so upper levels never grab
+// memory their own kernels do not profit from.  peak() is the exact high-water
+// mark of running a subtree with that schedule, INCLUDING its input, which a
+// level frees as soon as its last group has consumed it (ownership passes
+// down the recursion).  At every level the executor takes the largest R whose
+// subtree fits what the budget leaves (kTargets, R = 0: groups of one).
+constexpr int64_t kTargets[] = {4096, 2048, 1024, 512, 256, 128, 64, 0};
+constexpr int kNumTargets = sizeof(kTargets) / sizeof(kTargets[0]);
+
 struct Sched {
   const Model& m;
   const ForwardPlan& p;
-  bool cache;
-  std::vector<int64_t> need_min;
+  size_t L;
+  std::vector<std::vector<int64_t>> want;  // [target][layer]
+  mutable std::map<std::tuple<int, size_t, int64_t, bool>, int64_t> memo;
 
-  Sched(const Model& mm, const ForwardPlan& pp, bool c) : m(mm), p(pp), cache(c) {
-    const size_t L = m.net.layers.size();
-    need_min.assign(L + 1, 0);
-    for (size_t li = L; li-- > 0;) {
-      const Step st = step(li);
-      // the P entries this makes are processed one at a time below
-      need_min[li] = out_bytes(st, 1) + std::max(ws_bytes(st, 1), st.next < L ? need_min[st.next] : 0);
-    }
+  Sched(const Model& mm, const ForwardPlan& pp) : m(mm), p(pp), L(mm.net.layers.size()) {
+    want.assign(kNumTargets, std::vector<int64_t>(L + 1, 1));
+    for (int t = 0; t < kNumTargets; ++t)
+      for (size_t li = L; li-- > 0;) {
+        const Step st = step(li);
+        const int64_t next = st.next < L ? want[size_t(t)][st.next] : 1;
+        int64_t own = 1;
+        const Layer& l = m.net.layers[li];
+        if (l.kind == 0 && p.choice[li].algo == VXG_CONV_FFT && kTargets[t] > 0)
+          own = (kTargets[t] + p.choice[li].fft.tiles - 1) / p.choice[li].fft.tiles;
+        want[size_t(t)][li] = std::max(own, (next + st.P - 1) / st.P);
+      }
   }
 
   Step step(size_t li) const {
-    const size_t L = m.net.layers.size();
     const Layer& l = m.net.layers[li];
     if (l.kind == 0 && p.choice[li].algo == VXG_CONV_DIRECT && li + 1 < L &&
         m.net.layers[li + 1].kind == 1 && p.pool_mode[li + 1] == 1)
@@ -143,45 +158,50 @@ struct Sched {
     return Step{li, li + 1, false, P};
   }
 
-  int64_t out_bytes(const Step& st, int64_t g) const {
-    if (st.next >= m.net.layers.size()) return 0;  // leaves write the final buffer
-    return g * st.P * entry_bytes(p.shapes[st.next]);
-  }
+  int64_t in_bytes(size_t li, int64_t B) const { return li >= L ? 0 : B * entry_bytes(p.shapes[li]); }
 
-  // channel block of the fused direct conv: multiple of 16 maps
-  int64_t fused_block_bytes(const Step& st, int64_t g, int64_t cb) const {
-    const Shape& mid = p.shapes[st.li + 1];
-    return g * cb * mid.n.vol() * 4;
+  int64_t out_bytes(const Step& st, int64_t g) const {
+    if (st.next >= L) return 0;  // leaves write the final buffer
+    return g * st.P * entry_bytes(p.shapes[st.next]);
   }
 
   int64_t ws_bytes(const Step& st, int64_t g) const {
     const Layer& l = m.net.layers[st.li];
-    if (st.fused) return fused_block_bytes(st, g, std::min<int64_t>(16, l.fo));
+    if (st.fused) return g * std::min<int64_t>(16, l.fo) * p.shapes[st.li + 1].n.vol() * 4;
     if (l.kind != 0 || p.choice[st.li].algo != VXG_CONV_FFT) return 0;
     const LayerChoice& ch = p.choice[st.li];
-    const Shape& in = p.shapes[st.li];
     const int64_t M = g * ch.fft.tiles;
-    return fft_chunk_bytes(ch.fft, in.f, l.fo, std::min<int64_t>(M, 256));
+    return fft_chunk_bytes(ch.fft, p.shapes[st.li].f, l.fo, std::min<int64_t>(M, fft_reserved_rows()));
   }
 
-  int64_t group_need(const Step& st, int64_t g) const {
-    const size_t L = m.net.layers.size();
-    const int64_t rec = st.next < L ? need_min[st.next] : 0;
-    return out_bytes(st, g) + std::max(ws_bytes(st, g), rec);
+  int64_t group_of(int t, size_t li, int64_t B) const { return std::min(B, want[size_t(t)][li]); }
+
+  // high-water bytes of layers [li, L) on B entries (input included) under target t
+  int64_t peak(int t, size_t li, int64_t B, bool freeable) const {
+    if (li >= L || B <= 0) return 0;
+    const auto key = std::make_tuple(t, li, B, freeable);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    const Step st = step(li);
+    const int64_t G = group_of(t, li, B);
+    const int64_t in = in_bytes(li, B);
+    auto group = [&](int64_t g, bool last) {
+      const int64_t run = in + out_bytes(st, g) + ws_bytes(st, g);
+      const int64_t sub = peak(t, st.next, g * st.P, true);  // includes out(g)
+      const int64_t keep = (last && freeable) ? 0 : in;
+      return std::max(run, keep + sub);
+    };
+    int64_t r = group(G, G >= B);
+    if (B % G) r = std::max(r, group(B % G, true));
+    memo.emplace(key, r);
+    return r;
   }
 
-  // largest group (entries of layer li's input) whose step fits `avail`
-  int64_t choose(const Step& st, int64_t B, int64_t avail) const {
-    if (group_need(st, B) <= avail) return B;
-    int64_t lo = 1, hi = B;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) / 2;
-      if (group_need(st, mid) <= avail)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    return lo;
+  // largest target whose subtree fits `avail` on top of the (already held) input
+  int choose_target(size_t li, int64_t B, bool freeable, int64_t avail) const {
+    for (int t = 0; t < kNumTargets; ++t)
+      if (peak(t, li, B, freeable) - in_bytes(li, B) <= avail) return t;
+    return kNumTargets - 1;
   }
 };
 
@@ -229,16 +249,18 @@ struct Runner {
   int64_t final_off = 0;
   EventTimer& timer;
 
-  int64_t avail() const {
-    std::lock_guard<std::mutex> lk(m.c->mu);
-    return m.c->budget - m.c->current;
-  }
+  int64_t avail() const { return m.c->avail(); }
 
-  // run layers [li, L) on B entries of layer li's input at `in` (not owned)
-  void run(size_t li, const float* in, int64_t B) {
+  // run layers [li, L) on B entries of layer li's input at `in`; `owner`
+  // (optional) holds the input and is released once the last group consumed it
+  void run(size_t li, const float* in, int64_t B, DevBuf* owner) {
     const size_t L = m.net.layers.size();
     const Step st = sched.step(li);
-    const int64_t G = sched.choose(st, B, avail());
+    const int t = sched.choose_target(li, B, owner != nullptr, avail());
+    const int64_t G = sched.group_of(t, li, B);
+    if (trace_on())
+      std::fprintf(stderr, "[vxg] layer %zu: %lld entries, target rows %lld, groups of %lld\n", li,
+                   (long long)B, (long long)kTargets[t], (long long)G);
     const int64_t in_entry = entry_bytes(p.shapes[li]) / 4;
     for (int64_t b0 = 0; b0 < B; b0 += G) {
       const int64_t g = std::min(G, B - b0);
@@ -252,10 +274,11 @@ struct Runner {
         dst = out.as<float>();
       }
       exec(st, in + b0 * in_entry, g, dst);
+      if (owner && b0 + g >= B) owner->reset();  // stream-ordered free after the last reader
       if (leaf)
         final_off += g * st.P;
       else
-        run(st.next, dst, g * st.P);
+        run(st.next, dst, g * st.P, &out);
     }
   }
 
@@ -333,8 +356,14 @@ const float2* Model::spectra_for(int ci, const FftPlan& plan, bool /*cache*/) {
   throw invalid("model: unknown conv layer");
 }
 
-int64_t Model::plan_bytes(const ForwardPlan& p, bool cache) const {
-  Sched s(*this, p, cache);
+int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows) const {
+  Sched s(*this, p);
+  int t = kNumTargets - 1;
+  for (int i = 0; i < kNumTargets; ++i)
+    if (kTargets[i] <= target_rows) {
+      t = i;
+      break;
+    }
   const int64_t in = p.S * entry_bytes(p.shapes[0]);
   const int64_t frags = p.S * p.alpha * entry_bytes(p.shapes.back());
   const int64_t dense = p.S * p.f_out * p.dense.vol() * 4;
@@ -349,7 +378,7 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache) const {
       f = l.fo;
     }
   }
-  return in + frags + dense + spectra_bytes + s.need_min[0];
+  return frags + dense + spectra_bytes + std::max(in, s.peak(t, 0, p.S, false));
 }
 
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
@@ -363,8 +392,35 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
       spectra_for(conv_index[li], p.choice[li].fft, cache);
       timer.end(h);
     }
-  Runner r{*this, p, cache, Sched(*this, p, cache), frags.as<float>(), 0, timer};
-  r.run(0, d_in, p.S);
+  // The recursion runs inside one arena block taken from the pool: the pool
+  // maps it once and hands the same block back every forward, and the
+  // arena's coalescing free list keeps the large spectrum chunks contiguous
+  // (a bare stream-ordered pool fragments across forwards and has to unmap
+  // and remap). A big job gets everything the budget leaves.
+  {
+    Sched sched(*this, p);
+    const int64_t avail0 = c->avail();
+    const int64_t in0 = sched.in_bytes(0, p.S);
+    const int64_t top = sched.peak(0, 0, p.S, false) - in0;
+    int64_t arena_bytes = int64_t(double(avail0) * 0.995);
+    if (top <= avail0) arena_bytes = std::min(arena_bytes, top + top / 4 + (int64_t(256) << 20));
+    DevBuf arena_buf(c, arena_bytes);
+    Arena arena;
+    arena.reset(arena_buf.get(), arena_bytes);
+    struct Scope {
+      Ctx* c;
+      ~Scope() {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->arena = nullptr;
+      }
+    } scope{c};
+    {
+      std::lock_guard<std::mutex> lk(c->mu);
+      c->arena = &arena;
+    }
+    Runner r{*this, p, cache, Sched(*this, p), frags.as<float>(), 0, timer};
+    r.run(0, d_in, p.S, nullptr);
+  }
   if (!cache) spectra.clear();  // stream-ordered frees: recomputed by the next forward
   const size_t nwin = p.windows.size() / 3;
   if (nwin == 0) {

@@ -39,8 +39,9 @@ struct Model {
 
   Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr);
   ForwardPlan plan(int64_t S, V3 e, const int* conv_algos) const;
-  // bytes the forward needs (inputs + output included), or -1 if infeasible
-  int64_t plan_bytes(const ForwardPlan& p, bool cache_spectra) const;
+  // bytes the forward needs (inputs + output included) when every FFT layer
+  // gets contractions of at least target_rows rows (0: groups of one entry)
+  int64_t plan_bytes(const ForwardPlan& p, bool cache_spectra, int64_t target_rows = 0) const;
   // runs the forward on a device input; writes the dense output (device);
   // layer_seconds (optional) gets per-layer device time
   void forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache_spectra,

@@ -16,6 +16,10 @@
 // fastest: the 8 CTAs reading pieces of the same lines run concurrently and
 // share them through L2.
 //
+// With f == fo, Y may alias X (plan.inplace): a tile's Y pieces are exactly
+// the bytes its X chunks were read from, no other CTA touches them, and the
+// epilogue writes only after the tile's last MMA (hence every read) completed.
+//
 // Persistent, warp-specialised pipeline over a flat stream of (tile, K-chunk)
 // items and a 3-slot shared-memory ring (raw X chunk | pre-split W chunk |
 // split X chunk per slot), handshakes on mbarriers:

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--S", type=int, default=1)
+    ap.add_argument("--net", default="n537")
+    ap.add_argument("--extent", type=int, default=714)
     a = ap.parse_args()
     ctx = v.Context(0)
     res = {}
@@ -75,6 +77,30 @@ def main():
         t = timed(ctx, lambda: v.mpf_pool(x, (2, 2, 2), ctx))
         byt = 4.0 * 80 * (n ** 3 + 8 * 127 ** 3)
         res["mpf_80x255"] = {"s": t, "GBps": byt / t / 1e9}
+    if "net" in a.which:
+        from paper_1606_05688_b200.bundled_nets import NETS
+        net = v.parse_network_spec(NETS[a.net])
+        w = v.random_weights(net, 1)
+        m = v.Model(net, w, ctx)
+        e = a.extent
+        x = torch.rand((1, 1, e, e, e), device="cuda", generator=g) * 2 - 1
+        m.forward(x, cache_spectra=False)
+        ctx.sync()
+        ctx.profile(True)
+        t0 = time.perf_counter()
+        _, rep = m.forward(x, cache_spectra=False)
+        ctx.sync()
+        wall = time.perf_counter() - t0
+        ks = ctx.kernel_stats()
+        ctx.profile(False)
+        res["net_%s_%d" % (a.net, e)] = {
+            "seconds": rep.seconds, "wall": wall,
+            "layers": [round(s, 4) for s in rep.layer_seconds],
+            "kernels": {k: {"s": round(s["seconds"], 4), "n": s["launches"],
+                            "TFLOPs": round(s["flops"] / s["seconds"] / 1e12, 1) if s["flops"] else None,
+                            "GBps": round(s["bytes"] / s["seconds"] / 1e9) if s["bytes"] else None}
+                        for k, s in ks.items()}}
+        m.close()
     print(json.dumps(res, indent=1))
 
 
