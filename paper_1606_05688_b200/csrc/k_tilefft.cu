@@ -21,7 +21,10 @@
 // x planes are SX apart with SX = H (mod 16) so the y-line pass is conflict
 // free too.  One CTA owns one (tile, channel); every pass gives each thread
 // exactly one register-resident line (THREADS = T*H rounded up to a warp).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "async.cuh"
@@ -84,18 +87,33 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
     constexpr int NWARPS = C::THREADS / 32;
     const int lane = tid & 31, warp = tid >> 5;
     const int gz = oz + lane;
-    const bool zin = lane < T && gz < a.nz;
-    for (int x = warp; x < T; x += NWARPS) {
-      const int gx = ox + x;
-      const bool xin = zin && gx < a.nx;
-      const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
-      float* d = spf + 2 * (x * C::SX) + lane;
+    if (ox + T <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
+      // interior box (the common case): no bounds tests, one LDGSTS per row
+      if (lane < T) {
+        for (int x = warp; x < T; x += NWARPS) {
+          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.nz + gz;
+          float* d = spf + 2 * (x * C::SX) + lane;
+#pragma unroll 8
+          for (int y = 0; y < T; ++y) {
+            cp_async4(d + 2 * C::SY * y, g, true);
+            g += a.nz;
+          }
+        }
+      }
+    } else {
+      const bool zin = lane < T && gz < a.nz;
+      for (int x = warp; x < T; x += NWARPS) {
+        const int gx = ox + x;
+        const bool xin = zin && gx < a.nx;
+        const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
+        float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 4
-      for (int y = 0; y < T; ++y) {
-        const bool in = xin && oy + y < a.ny;
-        if (lane < T) cp_async4(d, in ? g : img, in);
-        g += a.nz;
-        d += 2 * C::SY;
+        for (int y = 0; y < T; ++y) {
+          const bool in = xin && oy + y < a.ny;
+          if (lane < T) cp_async4(d, in ? g : img, in);
+          g += a.nz;
+          d += 2 * C::SY;
+        }
       }
     }
   }
@@ -161,11 +179,22 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const int64_t wb_stride = a.mstride * a.f * lw;
   if (tid < T * C::H) {
     const float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
-    int w = tid;
+    if ((T * C::H) % 16 == 0 && lw == 16) {
+      // kx steps move whole 16-frequency lines: a fixed pointer increment
+      float2* o = dst + int64_t(tid >> 4) * wb_stride + (tid & 15);
+      const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
+#pragma unroll 8
+      for (int kx = 0; kx < T; ++kx) {
+        *o = s[kx * C::SX];
+        o += step;
+      }
+    } else {
+      int w = tid;
 #pragma unroll 4
-    for (int kx = 0; kx < T; ++kx) {
-      dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = s[kx * C::SX];
-      w += T * C::H;
+      for (int kx = 0; kx < T; ++kx) {
+        dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = s[kx * C::SX];
+        w += T * C::H;
+      }
     }
   }
   // zero tail up to a multiple of lw (read by the FFMA contraction only)
@@ -198,11 +227,21 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const int64_t wb_stride = a.mstride * a.fo * lw;
   if (tid < T * C::H) {
     float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
-    int w = tid;
+    if ((T * C::H) % 16 == 0 && lw == 16) {
+      const float2* g = src + int64_t(tid >> 4) * wb_stride + (tid & 15);
+      const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
+#pragma unroll 8
+      for (int kx = 0; kx < T; ++kx) {
+        cp_async8(s + kx * C::SX, g);
+        g += step;
+      }
+    } else {
+      int w = tid;
 #pragma unroll 4
-    for (int kx = 0; kx < T; ++kx) {
-      cp_async8(s + kx * C::SX, src + int64_t(w >> lshift) * wb_stride + (w & (lw - 1)));
-      w += T * C::H;
+      for (int kx = 0; kx < T; ++kx) {
+        cp_async8(s + kx * C::SX, src + int64_t(w >> lshift) * wb_stride + (w & (lw - 1)));
+        w += T * C::H;
+      }
     }
   }
   cp_async_commit();
