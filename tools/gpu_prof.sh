@@ -1,13 +1,16 @@
-# ncu evidence for the bench workload: launch list (per-launch durations) and
-# one --set full capture of each hot kernel.  Run through gpurun.
+# Round evidence: bench line, ncu launch list of the same bench command, and
+# --set full captures of the hot kernels on one deep 80->80 layer (kbench).
 set -x
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_bench.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"cgemm_tc_kernel|tile_fwd_kernel|tile_inv_kernel|mpf222_kernel|conv_direct_kernel" \
-  --launch-skip 40 --launch-count 8 -o gpurun_out/${TAG}_full -f \
-  python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"cgemm_tc_kernel|tile_fwd_kernel|tile_inv_kernel" --launch-skip 4 --launch-count 3 \
+  -o gpurun_out/${TAG}_layer -f python tools/kbench.py --which conv --S 64 --n 85 > gpurun_out/${TAG}_ncu_layer.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"mpf222_kernel|conv_direct_kernel" --launch-skip 2 --launch-count 2 \
+  -o gpurun_out/${TAG}_small -f python tools/kbench.py --which direct,mpf > gpurun_out/${TAG}_ncu_small.log 2>&1
 ls -la gpurun_out
