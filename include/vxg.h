@@ -116,6 +116,19 @@ int vxg_conv(vxg_ctx* ctx, int algo, int mem, const float* in, int64_t S, int64_
              const int64_t n[3], const float* kernels, int64_t fo, const int64_t k[3],
              const float* bias, int relu, float* out, vxg_audit* audit);
 
+/* The FFT convolution of vxg_conv with the plan pinned by the caller (parity
+ * tests, experiments): tile FFT size `tile` (must cover the kernel; one of
+ * 4 6 8 10 12 16 20 24 28 30 32), flags VXG_FFT_FFMA (fp32 FFMA contraction
+ * instead of tcgen05), VXG_FFT_SINGLE_CTA (no CTA-pair forward transform);
+ * spectra_budget > 0 caps the spectrum chunk buffers (bytes), forcing the
+ * multi-chunk path. */
+#define VXG_FFT_FFMA 1
+#define VXG_FFT_SINGLE_CTA 2
+int vxg_conv_fft_tiled(vxg_ctx* ctx, int mem, const float* in, int64_t S, int64_t f,
+                       const int64_t n[3], const float* kernels, int64_t fo, const int64_t k[3],
+                       const float* bias, int relu, float* out, int tile, int flags,
+                       int64_t spectra_budget);
+
 /* max_pool (layers.hpp:377-417): n % p == 0; NaN input -> VXG_INVALID. */
 int vxg_max_pool(vxg_ctx* ctx, int mem, const float* in, int64_t S, int64_t f,
                  const int64_t n[3], const int64_t p[3], float* out, vxg_audit* audit);

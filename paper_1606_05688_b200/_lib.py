@@ -78,6 +78,7 @@ def lib() -> C.CDLL:
                                      C.POINTER(C.c_double)]),
         "vxg_bench_ffma": (I, [P, C.POINTER(C.c_double)]),
         "vxg_conv": (I, [P, I, I, P, I64, I64, A, P, I64, A, P, I, P, C.POINTER(Audit)]),
+        "vxg_conv_fft_tiled": (I, [P, I, P, I64, I64, A, P, I64, A, P, I, P, I, I, I64]),
         "vxg_max_pool": (I, [P, I, P, I64, I64, A, A, P, C.POINTER(Audit)]),
         "vxg_mpf_pool": (I, [P, I, P, I64, I64, A, A, P, C.POINTER(Audit)]),
         "vxg_recombine": (I, [P, I, P, I64, I64, A, A, I64, I64, P]),

@@ -310,6 +310,34 @@ int vxg_conv(vxg_ctx* ctx, int algo, int mem, const float* in, int64_t S, int64_
   });
 }
 
+int vxg_conv_fft_tiled(vxg_ctx* ctx, int mem, const float* in, int64_t S, int64_t f,
+                       const int64_t n_[3], const float* kernels, int64_t fo, const int64_t k_[3],
+                       const float* bias, int relu, float* out, int tile, int flags,
+                       int64_t spectra_budget) {
+  return guard([&] {
+    Ctx* c = ctx_of(ctx);
+    const V3 n = v3_checked(n_, "vxg_conv_fft_tiled: n"), k = v3_checked(k_, "vxg_conv_fft_tiled: k");
+    need(in, "vxg_conv_fft_tiled: in");
+    need(kernels, "vxg_conv_fft_tiled: kernels");
+    need(bias, "vxg_conv_fft_tiled: bias");
+    need(out, "vxg_conv_fft_tiled: out");
+    require(S > 0 && f > 0 && n.positive(), "Shape5: all extents must be positive");
+    require(fo > 0 && k.positive(), "Shape5: all extents must be positive");
+    require(k.x <= n.x && k.y <= n.y && k.z <= n.z, "conv: kernel larger than image");
+    require(tile >= k.x && tile >= k.y && tile >= k.z, "vxg_conv_fft_tiled: tile smaller than the kernel");
+    const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
+    const FftPlan plan = plan_fft_forced(n, k, f, fo, S, tile, !(flags & VXG_FFT_FFMA),
+                                         !(flags & VXG_FFT_SINGLE_CTA));
+    In xin(c, mem, in, S * f * n.vol());
+    In win(c, mem, kernels, fo * f * k.vol());
+    In bin(c, mem, bias, fo);
+    Out o(c, mem, out, S * fo * no.vol());
+    conv_fft_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p, plan, nullptr,
+                    spectra_budget);
+    o.finish(c);
+  });
+}
+
 static int pool_common(vxg_ctx* ctx, int fragments, int mem, const float* in, int64_t S,
                        int64_t f, const int64_t n_[3], const int64_t p_[3], float* out,
                        vxg_audit* audit) {

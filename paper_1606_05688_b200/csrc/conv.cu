@@ -69,6 +69,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tiles = p.nt.vol();
     p.lw = 16;
     p.tc = tc;
+    p.pair = T == 32 && tile_pair_enabled();
     p.inplace = tc && f == fo;
     p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);
@@ -85,6 +86,17 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
   }
   if (best.T == 0) throw invalid("conv fft: no supported tile size covers the kernel");
   return best;
+}
+
+FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, bool tc, bool pair) {
+  FftPlan p = plan_fft(n, k, f, fo, S, T);
+  if (p.T != T) throw invalid("conv fft: unsupported tile size");
+  p.tc = tc && cgemm_tc_supported(f, fo);
+  p.pair = pair && T == 32;
+  p.lw = 16;
+  p.inplace = p.tc && f == fo;
+  p.nwp = tile_nwp(T, p.lw);
+  return p;
 }
 
 int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo) {
@@ -162,6 +174,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     fa.out = X.as<float2>();
     fa.scale = 1.f;
     fa.lw = plan.lw;
+    fa.pair = plan.pair;
     launch_tile_fwd(c, T, fa, mc * f);
 
     GemmArgs ga{};

@@ -22,6 +22,7 @@ struct FwdTileArgs {
   float scale;
   int kind = VXG_K_TILE_FWD; // instrumentation family (images or kernel spectra)
   int lw = 16;               // frequencies per contiguous chunk (16: FFMA path, 2: tensor cores)
+  bool pair = false;         // CTA-pair transform (tile_fwd_pair_kernel) where available
 };
 
 struct InvTileArgs {
@@ -54,6 +55,8 @@ struct GemmArgs {
 };
 
 extern const int kTileSizes[];
+// VXG_TILE_PAIR=0 disables the CTA-pair forward transform in planned layers
+bool tile_pair_enabled();
 extern const int kNumTileSizes;
 // frequencies of a T^3 tile padded to a multiple of the chunk width lw
 int64_t tile_nwp(int T, int lw);
@@ -76,12 +79,16 @@ struct FftPlan {
   int64_t tiles = 0;
   int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
+  bool pair = false;     // forward tile transform on a CTA pair (T = 32)
   bool inplace = false;  // tc with f == fo: Y overwrites X (each CTA tile reads
                          // exactly the bytes it later writes, see k_cgemm_tc.cu)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced = 0);
+// explicit variant (parity tests / experiments): tile size T, contraction and
+// forward-transform kernels chosen by the caller (tc only where supported)
+FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, bool tc, bool pair);
 
 // Device kernel spectra of one layer for tile size T: [w/lw][fo][f][lw], scaled 1/T^3.
 void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, int64_t f, V3 k,

@@ -205,6 +205,198 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   }
 }
 
+// ---- K1 / K2 on a CTA pair -------------------------------------------------------
+// The same transform split over a 2-CTA cluster so that a tile's spectrum
+// (139 KB at T = 32) becomes two 70 KB halves and two or three CTAs share an
+// SM: their load / FFT / store phases then overlap, which one CTA per SM
+// cannot do.  CTA rank r owns x-planes [r T/2, (r+1) T/2): it loads them, runs
+// their z (two-for-one, lines y and y + T/2) and y passes, then after a
+// cluster barrier transforms the x lines of its ky half, reading the other
+// half of every line from the peer's shared memory (DSMEM), and stores the
+// spectrum straight from registers.
+template <int T>
+struct PairCfg {
+  using C = TileCfg<T>;
+  static constexpr int HP = T / 2;                              // planes per CTA
+  static constexpr int SMEM = HP * C::SX * 8;
+  static constexpr int WORK = HP * C::H > HP * HP ? HP * C::H : HP * HP;
+  static constexpr int THREADS = ((WORK + 31) / 32) * 32;
+};
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t peer_addr(const void* local, unsigned peer) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(peer));
+  return r;
+}
+__device__ __forceinline__ float2 ld_peer(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int T>
+__global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdTileArgs a) {
+  using C = TileCfg<T>;
+  using P = PairCfg<T>;
+  constexpr int HP = P::HP;
+  constexpr int NWARPS = P::THREADS / 32;
+  extern __shared__ float2 sp[];
+  float* spf = reinterpret_cast<float*>(sp);
+  const unsigned r = cluster_rank();
+  const int64_t blk = blockIdx.x >> 1;
+  const int64_t j = blk % a.f;
+  const int64_t ml = blk / a.f;
+  const int64_t m = a.m0 + ml;
+  const int64_t s = m / a.tiles_per_img;
+  const int64_t t = m % a.tiles_per_img;
+  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
+  const int ox = tx * a.vx + int(r) * HP, oy = ty * a.vy, oz = tz * a.vz;
+  const float* img = a.src + (s * a.f + j) * a.img_stride;
+  const int tid = threadIdx.x;
+
+  // A0: this CTA's planes (raw) -> slots
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gz = oz + lane;
+    if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
+      if (lane < T) {
+        for (int x = warp; x < HP; x += NWARPS) {
+          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.nz + gz;
+          float* d = spf + 2 * (x * C::SX) + lane;
+#pragma unroll 8
+          for (int y = 0; y < T; ++y) {
+            cp_async4(d + 2 * C::SY * y, g, true);
+            g += a.nz;
+          }
+        }
+      }
+    } else {
+      const bool zin = lane < T && gz < a.nz;
+      for (int x = warp; x < HP; x += NWARPS) {
+        const int gx = ox + x;
+        const bool xin = zin && gx < a.nx;
+        const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
+        float* d = spf + 2 * (x * C::SX) + lane;
+#pragma unroll 4
+        for (int y = 0; y < T; ++y) {
+          const bool in = xin && oy + y < a.ny;
+          if (lane < T) cp_async4(d, in ? g : img, in);
+          g += a.nz;
+          d += 2 * C::SY;
+        }
+      }
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // A1: z r2c, lines (x, y) and (x, y + T/2) share one complex transform
+  if (tid < HP * HP) {
+    const int x = tid / HP, y = tid % HP;
+    float2* s1 = sp + x * C::SX + y * C::SY;
+    float2* s2 = s1 + HP * C::SY;
+    float2 zz[T];
+#pragma unroll
+    for (int q = 0; q < T / 2; ++q) {
+      const float2 r1 = s1[q], r2 = s2[q];
+      zz[2 * q] = make_float2(r1.x, r2.x);
+      zz[2 * q + 1] = make_float2(r1.y, r2.y);
+    }
+    fft<T, false>(zz);
+#pragma unroll
+    for (int k = 0; k < C::H; ++k) {
+      const float2 zk = zz[k];
+      const float2 zn = cconj(zz[(T - k) % T]);
+      const float2 d = csub(zk, zn);
+      s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
+      s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
+    }
+  }
+  __syncthreads();
+
+  // B: y lines (x, kz) of this CTA's planes
+  if (tid < HP * C::H) {
+    const int kz = tid % C::H, x = tid / C::H;
+    float2* base = sp + x * C::SX + kz;
+    float2 v[T];
+#pragma unroll
+    for (int y = 0; y < T; ++y) v[y] = base[y * C::SY];
+    fft<T, false>(v);
+#pragma unroll
+    for (int y = 0; y < T; ++y) base[y * C::SY] = v[y];
+  }
+  // both halves transformed along z and y
+  cluster_arrive();
+  cluster_wait();
+
+  // C: x lines (ky, kz) for ky in this CTA's half; x planes of the other half
+  // come from the peer
+  const int lw = a.lw, lshift = __ffs(lw) - 1;
+  float2* dst = a.out + (ml * a.f + j) * lw;
+  const int64_t wb_stride = a.mstride * a.f * lw;
+  float2 v[T];
+  const bool live = tid < HP * C::H;
+  if (live) {
+    const int ky = int(r) * HP + tid / C::H, kz = tid % C::H;
+    const float2* base = sp + ky * C::SY + kz;
+    const uint32_t pbase = peer_addr(base, r ^ 1u);
+    if (r == 0) {
+#pragma unroll
+      for (int x = 0; x < HP; ++x) {
+        v[x] = base[x * C::SX];
+        v[HP + x] = ld_peer(pbase + uint32_t(x * C::SX * 8));
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < HP; ++x) {
+        v[x] = ld_peer(pbase + uint32_t(x * C::SX * 8));
+        v[HP + x] = base[x * C::SX];
+      }
+    }
+  }
+  cluster_arrive();  // my reads of the peer are issued; it may exit after its own wait
+  if (live) {
+    fft<T, false>(v);
+    const int t0 = int(r) * HP * C::H + tid;  // w = kx*T*H + t0
+    if ((T * C::H) % 16 == 0 && lw == 16) {
+      float2* o = dst + int64_t(t0 >> 4) * wb_stride + (t0 & 15);
+      const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) {
+        *o = make_float2(v[kx].x * a.scale, v[kx].y * a.scale);
+        o += step;
+      }
+    } else {
+      int w = t0;
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) {
+        dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = make_float2(v[kx].x * a.scale, v[kx].y * a.scale);
+        w += T * C::H;
+      }
+    }
+  }
+  if (r == 0) {
+    const int nwp = ((C::NW + lw - 1) / lw) * lw;
+    if (tid < nwp - C::NW) {
+      const int w = C::NW + tid;
+      dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = make_float2(0.f, 0.f);
+    }
+  }
+  cluster_wait();  // the peer finished reading my planes
+}
+
 // ---- K4: inverse tile transform with crop + bias + ReLU ------------------------
 template <int T>
 __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
@@ -345,6 +537,31 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
+  if (a.pair && T == 32) {  // measured: faster than one CTA per tile at T = 32 only
+    using P = PairCfg<T>;
+    static bool pconf = false;
+    if (!pconf) {
+      VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_pair_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
+      pconf = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(2 * nblocks));
+    cfg.blockDim = dim3(P::THREADS);
+    cfg.dynamicSmemBytes = P::SMEM;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_fwd_pair_kernel<T>, a));
+    c->counted();
+    check_launch("tile_fwd_pair_kernel");
+    return;
+  }
   tile_fwd_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
   c->counted();
   check_launch("tile_fwd_kernel");
@@ -365,6 +582,14 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
 }
 
 }  // namespace
+
+bool tile_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VXG_TILE_PAIR");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
 
 // supported tile FFT sizes (even, {2,3,5,7}-smooth)
 const int kTileSizes[] = {4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32};

@@ -51,6 +51,7 @@ __all__ = [
     "NetworkSpec", "parse_network_spec", "format_network_spec", "field_of_view",
     "propagate_shapes", "random_weights", "fill_random", "execute", "Model",
     "ThroughputReport", "ParseError", "ResourceExhausted",
+    "conv_fft_tiled", "TILE_SIZES",
 ]
 
 
@@ -267,6 +268,28 @@ def conv_fft_staged(input, params, ctx=None):
 
 def conv_fft_task_parallel(input, params, ctx=None):
     return conv(input, params, L.CONV_FFT, ctx)
+
+
+def conv_fft_tiled(input, params: ConvLayerParams, tile: int, tensor_cores: bool = True,
+                   cta_pair: bool = True, spectra_budget: int = 0, ctx: Optional[Context] = None):
+    """The tiled FFT convolution with its plan pinned (vxg_conv_fft_tiled): tile FFT
+    size, tcgen05 vs FFMA contraction, CTA-pair vs one-CTA forward transform."""
+    ctx = ctx or default_context()
+    S, f = int(input.shape[0]), int(input.shape[1])
+    n = [int(v) for v in input.shape[2:]]
+    fo = params.features_out()
+    k = params.kernel_extents()
+    xi, wi, bi = _Arg(input), _Arg(params.kernels), _Arg(params.bias)
+    mem = _same_mem(xi, wi, bi)
+    out = _out_like(input, (S, fo) + tuple(n[a] - k[a] + 1 for a in range(3)))
+    flags = (0 if tensor_cores else 1) | (0 if cta_pair else 2)
+    check(lib().vxg_conv_fft_tiled(ctx.handle, mem, xi.ptr, S, f, i64s(n), wi.ptr, fo, i64s(k), bi.ptr,
+                                   1 if params.act == "relu" else 0, _ptr_of(out), int(tile), flags,
+                                   int(spectra_budget)))
+    return out
+
+
+TILE_SIZES = (4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32)
 
 
 def _pool(fn, input, p, P, ctx):

@@ -140,6 +140,47 @@ def test_conv_random_vs_oracle(oracle, ctx, case):
     assert rel_error(v.conv_fft_staged(x, p, ctx).output, want) <= 1e-4
 
 
+@pytest.mark.parametrize("variant", ["tc_pair", "tc_single", "ffma"])
+def test_conv_fft_every_tile_size_vs_oracle(oracle, ctx, variant):
+    """Every tile FFT size the planner may pick, each contraction and forward
+    transform kernel, with several tiles per axis, ragged edges, an anisotropic
+    kernel and a chunked spectrum (multi-launch) -- against the C oracle."""
+    import paper_1606_05688_b200 as v
+    S, f, fo = 2, 16, 16
+    rng = np.random.default_rng(11)
+    for T in v.TILE_SIZES:
+        k = (min(3, T), min(2, T), min(3, T))
+        n = (T + 7, 2 * T - 1, T + 3)
+        x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+        w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * np.prod(k)))).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+        want = oracle.conv(x, w, b, True)
+        p = v.ConvLayerParams(w, b, "relu")
+        got = v.conv_fft_tiled(x, p, T, tensor_cores=variant != "ffma", cta_pair=variant == "tc_pair",
+                               spectra_budget=3 * (f + fo) * T * T * (T // 2 + 1) * 8 + 4096, ctx=ctx)
+        assert rel_error(got, want) <= 1e-4, (T, variant, rel_error(got, want))
+
+
+def test_conv_fft_pair_kernel_matches_single(ctx):
+    """The CTA-pair forward transform computes the same transform as the one-CTA
+    kernel (T = 32, an 80 -> 80 layer: the bench's deep-layer shape).  The two
+    pair z lines differently in their two-for-one real transforms, so they
+    agree to fp32 rounding, not bitwise."""
+    import torch
+    import paper_1606_05688_b200 as v
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand((3, 80, 60, 61, 59), device="cuda", generator=gen) * 2 - 1
+    w = (torch.rand((80, 80, 5, 5, 5), device="cuda", generator=gen) * 2 - 1) * (3.0 / (80 * 125)) ** 0.5
+    b = (torch.rand((80,), device="cuda", generator=gen) * 2 - 1) * 0.1
+    p = v.ConvLayerParams(w.contiguous(), b.contiguous(), "relu")
+    a = v.conv_fft_tiled(x, p, 32, cta_pair=True, ctx=ctx)
+    c = v.conv_fft_tiled(x, p, 32, cta_pair=False, ctx=ctx)
+    d = v.conv_direct(x, p, ctx).output
+    scale = d.abs().max().item()
+    assert (a - c).abs().max().item() / scale <= 2e-6
+    assert (a - d).abs().max().item() / scale <= 1e-4
+
+
 def test_conv_fft_vs_direct_large(ctx):
     """Size-independent property at a realistic layer size: FFT == direct."""
     import torch
