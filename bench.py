@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--quick", action="store_true", help="small extent (profiling / smoke)")
+    ap.add_argument("--no-tune", action="store_true", help="modelled (not measured) layer planning")
     return ap.parse_args()
 
 
@@ -127,12 +128,12 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def pick_extent(model, budget_bytes, fov, hi=2048, stride=8, residue=2):
+def pick_extent(model, budget_bytes, fov, hi=2048, stride=8, residue=2, algos=None):
     """Largest admissible extent (e = residue mod stride) whose plan fits."""
     best = None
     e = hi - ((hi - residue) % stride)
     while e >= fov:
-        need = model.plan_bytes(1, e)
+        need = model.plan_bytes(1, e, algos)
         if 0 < need:
             # device input + dense output of the timed run live outside the plan
             extra = 4 * (e ** 3) + 4 * 3 * (e - fov + 1) ** 3
@@ -259,14 +260,43 @@ def main():
     ctx = v.Context(local, budget)
     model = v.Model(net, weights, ctx)
     budget_bytes = ctx.memory()["budget"]
-    if args.extent:
-        e = args.extent
-    elif args.quick:
-        e = 258
-    else:
-        e = pick_extent(model, budget_bytes * 0.97, fov)
+    nconv = sum(1 for l in net.layers if l[0] == "conv")
+
+    def choose(tuned):
+        """(extent, conv algos): the largest fitting patch, or -- with measured
+        layer costs -- the (patch, first-layer algorithm) pair of highest
+        estimated throughput among the largest few fitting patches: a direct
+        first layer fuses with the MPF after it (its full-resolution output
+        never exists) and so admits a larger patch than an FFT one."""
+        if args.extent:
+            return args.extent, None
+        if args.quick:
+            return 258, None
+        if not tuned:
+            return pick_extent(model, budget_bytes * 0.97, fov), None
+        best = None
+        for algos in (None, ["direct"] + ["auto"] * (nconv - 1)):
+            emax = pick_extent(model, budget_bytes * 0.97, fov, algos=algos)
+            if emax is None:
+                continue
+            for e in range(emax, max(fov, emax - 8 * 12) - 1, -8):
+                est = sum(l["seconds"] for l in model.plan_info(1, e, algos))
+                score = (e - fov + 1) ** 3 / est if est > 0 else 0
+                if best is None or score > best[0]:
+                    best = (score, e, algos)
+        return (best[1], best[2]) if best else (None, None)
+
+    e, algos = choose(False)
     if e is None:
         raise SystemExit("no admissible extent fits the HBM budget")
+    # measured-time layer planner: candidate tile sizes / direct timed on samples
+    # of each conv layer (outside the timed region), then the patch re-picked
+    t_tune = time.perf_counter()
+    if not args.no_tune:
+        model.tune(1, e)
+        e, algos = choose(True)
+    t_tune = time.perf_counter() - t_tune
+    plan = model.plan_info(1, e, algos)
     dense = e - fov + 1
     voxels = dense ** 3
 
@@ -279,7 +309,7 @@ def main():
     cache = bool(args.cache_spectra)
 
     def step():
-        model.forward(x_dev, out=out_dev, cache_spectra=cache)
+        model.forward(x_dev, out=out_dev, conv_algos=algos, cache_spectra=cache)
 
     for _ in range(args.warmup):
         step()
@@ -323,12 +353,12 @@ def main():
     out_host = torch.empty((1, 3, dense, dense, dense), dtype=torch.float32).pin_memory()
     xin = x_pin.numpy()
     oh = out_host.numpy()
-    model.forward(xin, out=oh, cache_spectra=cache)  # warm
+    model.forward(xin, out=oh, conv_algos=algos, cache_spectra=cache)  # warm
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        model.forward(xin, out=oh, cache_spectra=cache)
+        model.forward(xin, out=oh, conv_algos=algos, cache_spectra=cache)
     e2e_t = time.perf_counter() - t0
     if ws > 1:
         t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
@@ -396,6 +426,13 @@ def main():
                    "net": NET, "extent": e, "dense_out": dense, "global_batch": ws,
                    "parallelism": f"independent halo patches x{ws}",
                    "kernel_spectra": "cached across steps" if cache else "recomputed every step",
+                   "planner": ("modelled" if args.no_tune else
+                               f"measured (vxg_model_tune, {t_tune:.1f} s before the timed region)"),
+                   "planned_step_s": round(sum(l["seconds"] for l in plan), 4),
+                   "layers": " ".join(
+                       (f"L{l['layer']}:{l['algo']}" + (f"/T{l['T']}" + ("/tc" if l['tc'] else "/ffma")
+                                                          if l['algo'] == 'fft' else ""))
+                       if l["kind"] == "conv" else f"L{l['layer']}:mpf" for l in plan),
                    "l2": "inputs and activations >> 126 MB L2 (no flush needed)"},
         "e2e": e2e,
         "gpu_launches": launches,

@@ -212,6 +212,16 @@ int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S,
                       const int64_t e[3], const int* conv_algos, int cache_spectra,
                       float* dense_out, vxg_report* report);
 
+/* Measured-time planning: times the candidate tile sizes (and the direct
+ * kernel where it may compete) for every conv layer of the plan of (S, e) on
+ * sample inputs; later plans of this model choose per layer by measured cost. */
+int vxg_model_tune(vxg_model* model, int64_t S, const int64_t e[3]);
+/* The plan for (S, e) (conv_algos as vxg_model_forward): per layer 7 int64
+ * {kind (0 conv, 1 pool), algo (vxg_conv_algo), tile size T, tiles per entry,
+ * tensor cores, measured, estimated nanoseconds}; `out` holds 7 * layers. */
+int vxg_model_plan_info(vxg_model* model, int64_t S, const int64_t e[3], const int* conv_algos,
+                        int64_t* out);
+
 /* Peak HBM bytes vxg_model_forward would need for input extent e (planner
  * feasibility), or -1 when the shape chain is invalid. */
 int64_t vxg_model_plan_bytes(vxg_model* model, int64_t S, const int64_t e[3],

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
         "vxg_fill_random": (I, [P, I64, C.c_uint64]),
         "vxg_net_forward": (I, [P, P, P, I, P, I64, A, C.POINTER(I), P, C.POINTER(Report)]),
         "vxg_model_create": (I, [P, P, P, I, C.POINTER(P)]),
+        "vxg_model_tune": (I, [P, I64, A]),
+        "vxg_model_plan_info": (I, [P, I64, A, C.POINTER(I), A]),
         "vxg_model_free": (I, [P]),
         "vxg_model_forward": (I, [P, I, P, I64, A, C.POINTER(I), I, P, C.POINTER(Report)]),
         "vxg_model_plan_bytes": (I64, [P, I64, A, C.POINTER(I)]),

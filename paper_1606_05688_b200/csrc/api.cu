@@ -697,6 +697,35 @@ int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S, 
   });
 }
 
+int vxg_model_tune(vxg_model* model, int64_t S, const int64_t e[3]) {
+  return guard([&] {
+    need(model, "vxg_model_tune: model");
+    model->m->tune(S, v3_checked(e, "vxg_model_tune: e"));
+  });
+}
+
+int vxg_model_plan_info(vxg_model* model, int64_t S, const int64_t e[3], const int* conv_algos,
+                        int64_t* out) {
+  return guard([&] {
+    need(model, "vxg_model_plan_info: model");
+    need(out, "vxg_model_plan_info: out");
+    const ForwardPlan p = model->m->plan(S, v3_checked(e, "vxg_model_plan_info: e"), conv_algos);
+    for (size_t li = 0; li < model->m->net.layers.size(); ++li) {
+      const bool conv = model->m->net.layers[li].kind == 0;
+      const LayerChoice& ch = p.choice[li];
+      const bool fft = conv && ch.algo == VXG_CONV_FFT;
+      int64_t* o = out + 7 * li;
+      o[0] = conv ? 0 : 1;
+      o[1] = conv ? ch.algo : -1;
+      o[2] = fft ? ch.fft.T : 0;
+      o[3] = fft ? ch.fft.tiles : 0;
+      o[4] = fft && ch.fft.tc ? 1 : 0;
+      o[5] = ch.measured ? 1 : 0;
+      o[6] = int64_t(ch.seconds * 1e9);
+    }
+  });
+}
+
 int64_t vxg_model_plan_bytes(vxg_model* model, int64_t S, const int64_t e[3], const int* algos) {
   int64_t r = -1;
   const int st = guard([&] {

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <tuple>
 
@@ -67,6 +68,9 @@ ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos) const {
   for (size_t li = 0; li < L; ++li) {
     const Layer& l = net.layers[li];
     if (l.kind == 1) {
+      const Shape& pin = p.shapes[li];
+      const double elems = double(pin.s * S) * double(pin.f) * double(pin.n.vol());
+      p.choice[li].seconds = elems * (pool_elem > 0 ? pool_elem : 8.0 / 3e12);
       p.pool_mode[li] = modes[pi++];
       if (p.pool_mode[li] == 1)
         for (int a = 0; a < 3; ++a) p.windows.push_back(l.ext[a]);
@@ -78,19 +82,37 @@ ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos) const {
     require(algo == VXG_CONV_AUTO || algo == VXG_CONV_DIRECT || algo == VXG_CONV_FFT,
             "execute: unknown convolution algorithm");
     const int64_t B = in.s * S;
+    const V3 no{in.n.x - l.ext.x + 1, in.n.y - l.ext.y + 1, in.n.z - l.ext.z + 1};
     LayerChoice ch;
     bool fft_ok = true;
+    double direct = 2.0 * double(B) * double(in.f) * double(l.fo) * double(no.vol()) *
+                    double(l.ext.vol()) / 40e12;
+    auto mit = measured.find(ci);
     try {
       ch.fft = plan_fft(in.n, l.ext, in.f, l.fo, B);
+      if (mit != measured.end() && !mit->second.fft.empty()) {
+        // measured-time choice of the tile size
+        FftPlan best;
+        double best_s = 1e300;
+        for (const auto& kv : mit->second.fft) {
+          FftPlan q = plan_fft(in.n, l.ext, in.f, l.fo, B, kv.first);
+          q.cost = kv.second.first + kv.second.second * double(B) * double(q.tiles);
+          if (q.cost < best_s) {
+            best_s = q.cost;
+            best = q;
+          }
+        }
+        ch.fft = best;
+        ch.measured = true;
+      }
     } catch (const invalid&) {
       fft_ok = false;
     }
-    if (algo == VXG_CONV_AUTO) {
-      const V3 no{in.n.x - l.ext.x + 1, in.n.y - l.ext.y + 1, in.n.z - l.ext.z + 1};
-      const double direct = 2.0 * double(B) * double(in.f) * double(l.fo) * double(no.vol()) *
-                            double(l.ext.vol()) / 40e12;
+    if (mit != measured.end() && mit->second.direct_vox > 0)
+      direct = mit->second.direct_vox * double(B) * double(no.vol());
+    if (algo == VXG_CONV_AUTO)
       algo = (fft_ok && ch.fft.cost < direct) ? VXG_CONV_FFT : VXG_CONV_DIRECT;
-    }
+    ch.seconds = algo == VXG_CONV_FFT ? ch.fft.cost : direct;
     require(algo != VXG_CONV_FFT || fft_ok, "execute: kernel too large for the tiled FFT");
     ch.algo = algo;
     p.choice[li] = ch;
@@ -432,6 +454,135 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
                      int(nwin), d_dense, p.S);
   }
   timer.collect(layer_seconds, net.layers.size());
+}
+
+namespace {
+
+double time_on_stream(Ctx* c, const std::function<void()>& fn, int reps) {
+  cudaEvent_t a, b;
+  VXG_CUDA_CHECK(cudaEventCreate(&a));
+  VXG_CUDA_CHECK(cudaEventCreate(&b));
+  fn();  // warm (first launch configures the kernel)
+  double best = 1e300;
+  for (int r = 0; r < reps; ++r) {
+    VXG_CUDA_CHECK(cudaEventRecord(a, c->stream));
+    fn();
+    VXG_CUDA_CHECK(cudaEventRecord(b, c->stream));
+    VXG_CUDA_CHECK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    VXG_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, double(ms) * 1e-3);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return best;
+}
+
+__global__ void fill_sample_kernel(float* x, int64_t n, uint32_t seed) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t h = uint32_t(i) * 2654435761u ^ seed;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    x[i] = float(h & 0xFFFFFF) * (2.0f / 16777216.0f) - 1.0f;
+  }
+}
+
+void fill_sample(Ctx* c, float* x, int64_t n, uint32_t seed) {
+  fill_sample_kernel<<<grid_for(n, 256, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(x, n, seed);
+  check_launch("fill_sample_kernel");
+}
+
+}  // namespace
+
+// Measured-time planning (the reference's modelled seconds,
+// cost.cpp:52-78 / planner.cpp:70-86, replaced by timed kernels): for every
+// conv layer of the plan of (S, e), each admissible tile size T is timed on a
+// sample of the layer's own (f, fo, k) -- ~216 rows, 3 tiles per axis -- and
+// recorded as seconds per row; the direct kernel is timed too where the
+// model's estimate is within 4x of the FFT's.  plan() then scales the
+// per-row costs by each candidate's row count for the real extent.
+void Model::tune(int64_t S, V3 e) {
+  const ForwardPlan p0 = plan(S, e, nullptr);
+  for (size_t li = 0; li < net.layers.size(); ++li) {
+    const Layer& l = net.layers[li];
+    if (l.kind != 0) continue;
+    const int ci = conv_index[li];
+    if (measured.count(ci)) continue;
+    const Shape& in = p0.shapes[li];
+    const int64_t f = in.f, fo = l.fo;
+    const V3 k = l.ext;
+    LayerCosts lc;
+    const float* w = kern[size_t(ci)].as<float>();
+    const float* b = bias[size_t(ci)].as<float>();
+    for (int ti = 0; ti < kNumTileSizes; ++ti) {
+      const int T = kTileSizes[ti];
+      if (T < k.x || T < k.y || T < k.z || T < 8) continue;
+      V3 ns{3 * (T - k.x + 1) + k.x - 1, 3 * (T - k.y + 1) + k.y - 1, 3 * (T - k.z + 1) + k.z - 1};
+      const V3 nso{ns.x - k.x + 1, ns.y - k.y + 1, ns.z - k.z + 1};
+      // two sample sizes (~8 and ~40 entries of 27 tiles, the larger capped at
+      // ~12 GB of sample data) -> fixed seconds per launch + seconds per row
+      const int64_t per_entry = (f * ns.vol() + fo * nso.vol()) * 4 +
+                                27 * (f + fo) * tile_nwp(T, 16) * 8;
+      const int64_t S2 = std::max<int64_t>(9, std::min<int64_t>(40, (int64_t(12) << 30) / per_entry));
+      const int64_t S1 = std::max<int64_t>(1, S2 / 5);
+      FftPlan fp = plan_fft(ns, k, f, fo, S2, T);
+      DevBuf x(c, S2 * f * ns.vol() * 4);
+      DevBuf y(c, S2 * fo * nso.vol() * 4);
+      fill_sample(c, x.as<float>(), S2 * f * ns.vol(), 12345u + uint32_t(T));
+      DevBuf ws(c, kernel_spectra_bytes(fp, f, fo));
+      compute_kernel_spectra(c, T, fp.tc, w, fo, f, k, ws.as<float2>());
+      double t[2];
+      const int64_t Ss[2] = {S1, S2};
+      for (int q = 0; q < 2; ++q)
+        t[q] = time_on_stream(c, [&] {
+          conv_fft_device(c, x.as<float>(), Ss[q], f, ns, w, fo, k, b, l.relu, y.as<float>(), fp,
+                          ws.as<float2>(), 0);
+        }, 2);
+      const double rows1 = double(S1 * fp.tiles), rows2 = double(S2 * fp.tiles);
+      const double per_row = std::max(0.0, (t[1] - t[0]) / (rows2 - rows1));
+      lc.fft[T] = {std::max(0.0, t[0] - per_row * rows1), per_row};
+    }
+    // direct convolution, where it might compete
+    {
+      const LayerChoice& ch = p0.choice[li];
+      const V3 no{in.n.x - k.x + 1, in.n.y - k.y + 1, in.n.z - k.z + 1};
+      const double dmodel = 2.0 * double(f) * fo * double(no.vol()) * double(k.vol()) / 40e12;
+      double best_fft = 1e300;
+      for (const auto& kv : lc.fft) {
+        const FftPlan q = plan_fft(in.n, k, f, fo, 1, kv.first);
+        best_fft = std::min(best_fft, kv.second.first + kv.second.second * double(q.tiles));
+      }
+      if (ch.algo == VXG_CONV_DIRECT || dmodel < 4.0 * best_fft) {
+        const V3 ns{40 + k.x - 1, 40 + k.y - 1, 40 + k.z - 1};
+        DevBuf x(c, f * ns.vol() * 4), y(c, fo * 40 * 40 * 40 * 4);
+        fill_sample(c, x.as<float>(), f * ns.vol(), 777u);
+        const double t = time_on_stream(c, [&] {
+          conv_direct_device(c, x.as<float>(), 1, f, ns, w, fo, k, b, l.relu, y.as<float>());
+        }, 2);
+        lc.direct_vox = t / (40.0 * 40.0 * 40.0);
+      }
+    }
+    if (trace_on()) {
+      std::fprintf(stderr, "[vxg] tune layer %zu (f=%lld fo=%lld k=%lld):", li, (long long)f,
+                   (long long)fo, (long long)k.x);
+      for (const auto& kv : lc.fft)
+        std::fprintf(stderr, " T%d %.3gms+%.3gns/row", kv.first, kv.second.first * 1e3, kv.second.second * 1e9);
+      if (lc.direct_vox > 0) std::fprintf(stderr, " direct %.3gns/vox", lc.direct_vox * 1e9);
+      std::fprintf(stderr, "\n");
+    }
+    measured[ci] = lc;
+  }
+  if (pool_elem < 0) {
+    // MPF (p = 2) on a sample: seconds per input element
+    const int64_t f = 80, n = 127;
+    const V3 nv{n, n, n}, pw{2, 2, 2};
+    DevBuf x(c, f * nv.vol() * 4), y(c, 8 * f * 63 * 63 * 63 * 4);
+    fill_sample(c, x.as<float>(), f * nv.vol(), 99u);
+    const double t = time_on_stream(c, [&] { launch_mpf(c, x.as<float>(), 1, f, nv, pw, y.as<float>()); }, 2);
+    pool_elem = t / double(f * nv.vol());
+  }
 }
 
 }  // namespace vxg

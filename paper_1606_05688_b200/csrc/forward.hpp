@@ -15,6 +15,8 @@ namespace vxg {
 struct LayerChoice {
   int algo = VXG_CONV_AUTO;  // resolved to DIRECT or FFT
   FftPlan fft;
+  bool measured = false;     // tile size chosen from measured costs (Model::tune)
+  double seconds = 0;        // estimated seconds of the layer (measured costs, else the model)
 };
 
 // Per-forward plan: shapes per layer boundary for ONE input entry, resolved
@@ -30,12 +32,24 @@ struct ForwardPlan {
   int64_t alpha = 1;                  // fragments per input entry
 };
 
+// Measured per-layer costs (Model::tune): seconds per spectrum row of the
+// tiled FFT convolution for each tile size, seconds per output voxel of the
+// direct convolution; keyed by the layer's (f, fo, k).
+struct LayerCosts {
+  // T -> {fixed seconds per launch, seconds per (batch, tile) row}: fitted
+  // from two sample sizes (the fixed part is mostly the kernel-spectrum stream)
+  std::map<int, std::pair<double, double>> fft;
+  double direct_vox = -1;         // seconds per output voxel (all maps), < 0: not measured
+};
+
 struct Model {
   Ctx* c = nullptr;
   Net net;
   std::vector<int> conv_index;        // layer -> conv ordinal or -1
   std::vector<DevBuf> kern, bias;     // per conv ordinal
   std::map<std::pair<int, int>, DevBuf> spectra;  // (conv ordinal, T) -> kernel spectra
+  std::map<int, LayerCosts> measured;             // conv ordinal -> measured costs
+  double pool_elem = -1;                          // measured MPF seconds per input element
 
   Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr);
   ForwardPlan plan(int64_t S, V3 e, const int* conv_algos) const;
@@ -47,6 +61,10 @@ struct Model {
   void forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache_spectra,
                std::vector<double>* layer_seconds);
   const float2* spectra_for(int ci, const FftPlan& plan, bool cache);
+  // Measured-time planning: times every admissible tile size (and the direct
+  // kernel where the model gives it a chance) on sample inputs of each conv
+  // layer's real (f, fo, k); plan() then picks per layer by measured cost.
+  void tune(int64_t S, V3 e);
 };
 
 }  // namespace vxg

@@ -560,6 +560,29 @@ class Model:
         e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]
         return int(lib().vxg_model_plan_bytes(self._p, int(S), i64s(e), _algos(self.net, conv_algos)))
 
+    def tune(self, S: int, e):
+        """Measured-time planning for input (S, f_in, e) (vxg_model_tune)."""
+        e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]
+        check(lib().vxg_model_tune(self._p, int(S), i64s(e)))
+
+    def plan_info(self, S: int, e, conv_algos=None):
+        """Per layer: {"kind", "algo", "T", "tiles", "tc", "measured", "seconds"} of the
+        plan for (S, e); "seconds" is the planner's estimate (measured costs after tune())."""
+        e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]
+        n = self.net.layer_count
+        buf = (C.c_int64 * (7 * n))()
+        check(lib().vxg_model_plan_info(self._p, int(S), i64s(e), _algos(self.net, conv_algos), buf))
+        algo = {L.CONV_DIRECT: "direct", L.CONV_FFT: "fft"}
+        out = []
+        for i in range(n):
+            k, a, T, tiles, tc, meas, ns = buf[7 * i:7 * i + 7]
+            if k == 0:
+                out.append({"layer": i, "kind": "conv", "algo": algo.get(a, str(a)), "T": T,
+                            "tiles": tiles, "tc": bool(tc), "measured": bool(meas), "seconds": ns * 1e-9})
+            else:
+                out.append({"layer": i, "kind": "pool", "seconds": ns * 1e-9})
+        return out
+
     def forward(self, input, out=None, conv_algos=None, cache_spectra=True):
         S = int(input.shape[0])
         e = [int(v) for v in input.shape[2:]]

@@ -48,6 +48,31 @@ def test_bundled_nets(golden, ctx, name):
     assert rep.seconds > 0 and len(rep.layer_seconds) == v.parse_network_spec(m["text"]).layer_count
 
 
+@pytest.mark.parametrize("name", ["n537", "n726"])
+def test_measured_planner_keeps_parity(golden, ctx, name):
+    """The measured-time planner (Model.tune) only changes tile sizes and FFT vs
+    direct: the bundled net still matches the fp64 reference, every conv layer
+    reports a measured choice and a positive time estimate."""
+    import paper_1606_05688_b200 as v
+    meta = json.loads((GOLD / "nets_bundled.json").read_text())
+    g = golden("nets_bundled")
+    m = meta[name]
+    net = v.parse_network_spec(m["text"])
+    w = v.random_weights(net, m["wseed"])
+    e = tuple(m["extent"])
+    x = v.fill_random(int(np.prod(e)), m["iseed"]).reshape((1, 1) + e)
+    model = v.Model(net, w, ctx)
+    model.tune(1, e)
+    plan = model.plan_info(1, e)
+    convs = [l for l in plan if l["kind"] == "conv"]
+    assert convs and all(l["seconds"] > 0 for l in plan)
+    assert all(l["measured"] for l in convs if l["algo"] == "fft")
+    for algos in (None, ["direct"] + ["auto"] * (len(convs) - 1)):
+        out, rep = model.forward(x, conv_algos=algos)
+        assert rel_error(out, g[f"{name}_out64"]) <= TOL, algos
+    model.close()
+
+
 def test_forward_independent_of_budget_and_algorithm(ctx):
     """Any feasible execution gives the same dense result (execute.hpp:384-386):
     fragment groups forced small by the budget reproduce the unconstrained run
