@@ -70,6 +70,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.lw = 16;
     p.tc = tc;
     p.pair = T == 32 && tile_pair_enabled();
+    p.inv_pair = (T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled();  // measured wins
     p.inplace = tc && f == fo;
     p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);
@@ -93,6 +94,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   if (p.T != T) throw invalid("conv fft: unsupported tile size");
   p.tc = tc && cgemm_tc_supported(f, fo);
   p.pair = pair && T == 32;
+  p.inv_pair = pair && T >= 24;  // tests: every pair-capable size
   p.lw = 16;
   p.inplace = p.tc && f == fo;
   p.nwp = tile_nwp(T, p.lw);
@@ -206,6 +208,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ia.bias = bias;
     ia.relu = relu ? 1 : 0;
     ia.lw = plan.lw;
+    ia.pair = plan.inv_pair;
     launch_tile_inv(c, T, ia, mc * fo);
   }
 }

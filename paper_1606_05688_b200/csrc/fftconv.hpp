@@ -40,6 +40,7 @@ struct InvTileArgs {
   const float* bias;
   int relu;
   int lw = 16;
+  bool pair = false;         // CTA-pair transform (tile_inv_pair_kernel)
 };
 
 struct GemmArgs {
@@ -57,6 +58,7 @@ struct GemmArgs {
 extern const int kTileSizes[];
 // VXG_TILE_PAIR=0 disables the CTA-pair forward transform in planned layers
 bool tile_pair_enabled();
+bool inv_pair_enabled();  // VXG_INV_PAIR=0 disables the CTA-pair inverse
 extern const int kNumTileSizes;
 // frequencies of a T^3 tile padded to a multiple of the chunk width lw
 int64_t tile_nwp(int T, int lw);
@@ -80,6 +82,7 @@ struct FftPlan {
   int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
   bool pair = false;     // forward tile transform on a CTA pair (T = 32)
+  bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
   bool inplace = false;  // tc with f == fo: Y overwrites X (each CTA tile reads
                          // exactly the bytes it later writes, see k_cgemm_tc.cu)
   int64_t nwp = 0;   // padded frequencies per (row, channel)

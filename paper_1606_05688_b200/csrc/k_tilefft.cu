@@ -528,6 +528,152 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   }
 }
 
+// ---- K4 on a CTA pair ---------------------------------------------------------
+// Rank r transforms the x lines of its ky half straight from HBM into registers
+// (one coalesced 8-byte load per line element, 32 in flight per thread),
+// writes each result to the CTA owning its x plane (local or DSMEM), and after
+// a cluster barrier runs the y pass, the z c2r with bias + activation and the
+// store for the crop planes it owns.
+__device__ __forceinline__ void st_peer(uint32_t addr, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};\n" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+
+template <int T>
+__global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvTileArgs a) {
+  using C = TileCfg<T>;
+  using P = PairCfg<T>;
+  constexpr int HP = P::HP;
+  constexpr int NWARPS = P::THREADS / 32;
+  extern __shared__ float2 sp[];
+  float* spf = reinterpret_cast<float*>(sp);
+  const unsigned r = cluster_rank();
+  const int64_t blk = blockIdx.x >> 1;
+  const int64_t i = blk % a.fo;
+  const int64_t ml = blk / a.fo;
+  const int64_t m = a.m0 + ml;
+  const int64_t s = m / a.tiles_per_img;
+  const int64_t t = m % a.tiles_per_img;
+  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
+  const int tid = threadIdx.x;
+  const int x0 = int(r) * HP;  // my planes [x0, x0 + HP)
+
+  // A+B: x lines (ky in my half, all kz) from HBM, inverse transform, scatter
+  if (tid < HP * C::H) {
+    const int lw = a.lw, lshift = __ffs(lw) - 1;
+    const float2* src = a.spec + (ml * a.fo + i) * lw;
+    const int64_t wb_stride = a.mstride * a.fo * lw;
+    const int t0 = x0 * C::H + tid;  // ky * H + kz, ky = x0 + tid / H
+    float2 v[T];
+    if ((T * C::H) % 16 == 0 && lw == 16) {
+      const float2* g = src + int64_t(t0 >> 4) * wb_stride + (t0 & 15);
+      const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) v[kx] = __ldg(g + kx * step);
+    } else {
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) {
+        const int w = kx * T * C::H + t0;
+        v[kx] = __ldg(src + int64_t(w >> lshift) * wb_stride + (w & (lw - 1)));
+      }
+    }
+    fft<T, true>(v);
+    const int ky = x0 + tid / C::H, kz = tid % C::H;
+    float2* base = sp + ky * C::SY + kz;
+    const uint32_t pbase = peer_addr(base, r ^ 1u);
+    if (r == 0) {
+#pragma unroll
+      for (int x = 0; x < HP; ++x) {
+        base[x * C::SX] = v[x];
+        st_peer(pbase + uint32_t(x * C::SX * 8), v[HP + x]);
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < HP; ++x) {
+        st_peer(pbase + uint32_t(x * C::SX * 8), v[x]);
+        base[x * C::SX] = v[HP + x];
+      }
+    }
+  }
+  cluster_arrive();
+  cluster_wait();
+
+  // crop planes owned here
+  const int xa = max(a.cx, x0), xb = min(a.cx + a.vx, x0 + HP);
+  const int nxl = max(0, xb - xa);
+
+  // C: y lines for my crop planes
+  if (tid < nxl * C::H) {
+    const int kz = tid % C::H, xl = xa - x0 + tid / C::H;
+    float2* base = sp + xl * C::SX + kz;
+    float2 v[T];
+#pragma unroll
+    for (int y = 0; y < T; ++y) v[y] = base[y * C::SY];
+    fft<T, true>(v);
+#pragma unroll
+    for (int y = 0; y < T; ++y) base[y * C::SY] = v[y];
+  }
+  __syncthreads();
+
+  // D: z c2r for crop (x, y) of my planes, pairs (l, l + half); bias + activation
+  const int L = nxl * a.vy;
+  const int half = (L + 1) / 2;
+  for (int l1 = tid; l1 < half; l1 += P::THREADS) {
+    const float bias = __ldg(a.bias + i);
+    const int l2 = l1 + half;
+    const bool has2 = l2 < L;
+    float2* s1 = sp + (xa - x0 + l1 / a.vy) * C::SX + (a.cy + l1 % a.vy) * C::SY;
+    float2* s2 = has2 ? sp + (xa - x0 + l2 / a.vy) * C::SX + (a.cy + l2 % a.vy) * C::SY : s1;
+    float2 zz[T];
+#pragma unroll
+    for (int k = 0; k < C::H; ++k) {
+      const float2 A = s1[k];
+      const float2 B = has2 ? s2[k] : make_float2(0.f, 0.f);
+      zz[k] = make_float2(A.x - B.y, A.y + B.x);  // A + iB
+    }
+#pragma unroll
+    for (int k = C::H; k < T; ++k) {
+      const float2 A = s1[T - k];
+      const float2 B = has2 ? s2[T - k] : make_float2(0.f, 0.f);
+      zz[k] = make_float2(A.x + B.y, -A.y + B.x);  // conj(A) + i conj(B)
+    }
+    fft<T, true>(zz);
+    float* r1 = spf + 2 * (s1 - sp);
+    float* r2 = spf + 2 * (s2 - sp);
+#pragma unroll
+    for (int z = 0; z < T; ++z) {
+      if (z >= a.cz && z < a.cz + a.vz) {
+        const float v1 = zz[z].x + bias;
+        r1[z] = a.relu ? (v1 > 0.f ? v1 : 0.f) : v1;  // activate (layers.hpp:105-108)
+        if (has2) {
+          const float v2 = zz[z].y + bias;
+          r2[z] = a.relu ? (v2 > 0.f ? v2 : 0.f) : v2;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // E: store my crop planes, clipped to the output image
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gy0 = ty * a.vy, gz = tz * a.vz + lane;
+    const bool zin = lane < a.vz && gz < a.onz;
+    const int ylim = min(a.vy, a.ony - gy0);
+    for (int xx = warp; xx < nxl; xx += NWARPS) {
+      const int gx = tx * a.vx + (xa - a.cx) + xx;
+      if (!zin || gx >= a.onx) continue;
+      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.onz + gz;
+      const float* rr = spf + 2 * ((xa - x0 + xx) * C::SX + a.cy * C::SY) + a.cz + lane;
+#pragma unroll 4
+      for (int y = 0; y < ylim; ++y) {
+        *o = *rr;
+        o += a.onz;
+        rr += 2 * C::SY;
+      }
+    }
+  }
+}
+
 template <int T>
 void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
@@ -576,6 +722,31 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
+  if (a.pair && T >= 24) {
+    using P = PairCfg<T>;
+    static bool pconf = false;
+    if (!pconf) {
+      VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_pair_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
+      pconf = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(2 * nblocks));
+    cfg.blockDim = dim3(P::THREADS);
+    cfg.dynamicSmemBytes = P::SMEM;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair_kernel<T>, a));
+    c->counted();
+    check_launch("tile_inv_pair_kernel");
+    return;
+  }
   tile_inv_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
   c->counted();
   check_launch("tile_inv_kernel");
@@ -586,6 +757,14 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
 bool tile_pair_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("VXG_TILE_PAIR");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
+bool inv_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VXG_INV_PAIR");
     return !(e && std::strcmp(e, "0") == 0);
   }();
   return on;
