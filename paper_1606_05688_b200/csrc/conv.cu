@@ -69,7 +69,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tiles = p.nt.vol();
     p.lw = 16;
     p.tc = tc;
-    p.pair = T == 32 && tile_pair_enabled();
+    p.pair = (T == 32 || T == 24) && tile_pair_enabled();  // measured wins (other T: one CTA is as fast)
     p.inv_pair = (T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled();  // measured wins
     p.inplace = tc && f == fo;
     p.nwp = tile_nwp(T, p.lw);
@@ -93,7 +93,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   FftPlan p = plan_fft(n, k, f, fo, S, T);
   if (p.T != T) throw invalid("conv fft: unsupported tile size");
   p.tc = tc && cgemm_tc_supported(f, fo);
-  p.pair = pair && T == 32;
+  p.pair = pair && T >= 24;  // tests: every pair-capable size
   p.inv_pair = pair && T >= 24;  // tests: every pair-capable size
   p.lw = 16;
   p.inplace = p.tc && f == fo;

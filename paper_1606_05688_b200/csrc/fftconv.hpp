@@ -81,7 +81,7 @@ struct FftPlan {
   int64_t tiles = 0;
   int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
-  bool pair = false;     // forward tile transform on a CTA pair (T = 32)
+  bool pair = false;     // forward tile transform on a CTA pair (T >= 24)
   bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
   bool inplace = false;  // tc with f == fo: Y overwrites X (each CTA tile reads
                          // exactly the bytes it later writes, see k_cgemm_tc.cu)

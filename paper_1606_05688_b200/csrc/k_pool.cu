@@ -314,27 +314,40 @@ struct RecGeom {
   int64_t scale[8];          // fragments per unit of window w's index
 };
 
+// Row-wise gather: one CTA per dense row (s, map, dx, dy).  The fragment a
+// dense voxel comes from is b(s) + fx(dx) + fy(dy) + fz(dz % sz) with each
+// term a sum over the windows (recombine_fragments' index decomposition,
+// layers.hpp:493-517); the z term is tabulated once per CTA in shared memory,
+// so the inner loop is one table read, one gather and one coalesced store.
+__device__ __forceinline__ int64_t frag_term(const RecGeom& g, int64_t off, int axis) {
+  int64_t b = 0;
+  for (int w = 0; w < g.nwin; ++w) {
+    const int64_t o = (off / g.pre[w][axis]) % g.win[w][axis];
+    const int64_t mul = axis == 0 ? int64_t(g.win[w][1]) * g.win[w][2] : (axis == 1 ? g.win[w][2] : 1);
+    b += o * mul * g.scale[w];
+  }
+  return b;
+}
+
 __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict__ frag,
                                                         float* __restrict__ dense, RecGeom g) {
-  const int64_t del = g.dx * g.dy * g.dz;
-  const int64_t total = g.S0 * g.f * del;
+  __shared__ int64_t ztab[256];  // fragment-offset term per dz % sz (sz <= 256)
+  const int64_t row = blockIdx.x;  // (s, fm, dx, dy)
+  const int64_t dy = row % g.dy;
+  const int64_t dx = (row / g.dy) % g.dx;
+  const int64_t sf = row / (g.dy * g.dx);
+  const int64_t fm = sf % g.f, s = sf / g.f;
+  for (int o = threadIdx.x; o < g.sz; o += blockDim.x) ztab[o] = frag_term(g, o, 2);
+  __syncthreads();
   const int64_t nel = g.nx * g.ny * g.nz;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t v = t % del;
-    const int64_t sf = t / del;
-    const int64_t fm = sf % g.f, s = sf / g.f;
-    const int64_t dz = v % g.dz, dy = (v / g.dz) % g.dy, dx = v / (g.dz * g.dy);
-    const int64_t offx = dx % g.sx, offy = dy % g.sy, offz = dz % g.sz;
-    int64_t b = s * g.alpha;
-    for (int w = 0; w < g.nwin; ++w) {
-      const int64_t ox = (offx / g.pre[w][0]) % g.win[w][0];
-      const int64_t oy = (offy / g.pre[w][1]) % g.win[w][1];
-      const int64_t oz = (offz / g.pre[w][2]) % g.win[w][2];
-      b += ((ox * g.win[w][1] + oy) * g.win[w][2] + oz) * g.scale[w];
-    }
-    const int64_t x = dx / g.sx, y = dy / g.sy, z = dz / g.sz;
-    dense[t] = __ldg(frag + (b * g.f + fm) * nel + (x * g.ny + y) * g.nz + z);
+  const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
+  const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.nz;
+  float* dst = dense + row * g.dz;
+  const int sz = int(g.sz);
+  const int64_t fstride = g.f * nel;
+  for (int dz = threadIdx.x; dz < g.dz; dz += blockDim.x) {
+    const int oz = dz % sz;
+    dst[dz] = __ldg(src + (bxy + ztab[oz]) * fstride + dz / sz);
   }
 }
 
@@ -410,8 +423,10 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
   const int64_t total = S0 * f * g.dx * g.dy * g.dz;
   if (total == 0) return;
   KScope ks(c, VXG_K_RECOMBINE, 0.0, 8.0 * double(total));
-  recombine_kernel<<<grid_for(total, 256, int64_t(c->num_sms) * 32), 256, 0, c->stream>>>(
-      frag, dense, g);
+  require(g.sz <= 256, "recombine: z stride product above 256");
+  const int64_t rows = S0 * f * g.dx * g.dy;
+  require(rows < (int64_t(1) << 31), "recombine: too many dense rows");
+  recombine_kernel<<<unsigned(rows), 256, 0, c->stream>>>(frag, dense, g);
   c->counted();
   check_launch("recombine_kernel");
 }

@@ -683,7 +683,7 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
-  if (a.pair && T == 32) {  // measured: faster than one CTA per tile at T = 32 only
+  if (a.pair && T >= 24) {
     using P = PairCfg<T>;
     static bool pconf = false;
     if (!pconf) {

@@ -57,6 +57,14 @@ __all__ = [
 
 # ---- context ---------------------------------------------------------------------------
 
+
+def _finish(ctx, mem):
+    """Layer primitives are externally synchronous (the reference's contract,
+    SPEC.md:283): device-pointer calls are stream-ordered inside the library,
+    so wait for them before handing results back to the caller's streams."""
+    if mem == L.MEM_DEVICE:
+        ctx.sync()
+
 _live_contexts = weakref.WeakSet()
 _live_models = weakref.WeakSet()
 
@@ -250,6 +258,7 @@ def conv(input, params: ConvLayerParams, algo: int = L.CONV_AUTO, ctx: Optional[
     au = L.Audit()
     check(lib().vxg_conv(ctx.handle, int(algo), mem, xi.ptr, S, f, i64s(n), wi.ptr, fo, i64s(k),
                          bi.ptr, 1 if params.act == "relu" else 0, _ptr_of(out), C.byref(au)))
+    _finish(ctx, mem)
     return LayerResult(out, MemoryAudit(au.peak, au.model))
 
 
@@ -286,6 +295,7 @@ def conv_fft_tiled(input, params: ConvLayerParams, tile: int, tensor_cores: bool
     check(lib().vxg_conv_fft_tiled(ctx.handle, mem, xi.ptr, S, f, i64s(n), wi.ptr, fo, i64s(k), bi.ptr,
                                    1 if params.act == "relu" else 0, _ptr_of(out), int(tile), flags,
                                    int(spectra_budget)))
+    _finish(ctx, mem)
     return out
 
 
@@ -305,6 +315,7 @@ def _pool(fn, input, p, P, ctx):
     out = _out_like(input, (S * (int(np.prod(p)) if P else 1), f) + tuple(n[a] // p[a] for a in range(3)))
     au = L.Audit()
     check(fn(ctx.handle, xi.mem, xi.ptr, S, f, i64s(n), i64s(p), _ptr_of(out), C.byref(au)))
+    _finish(ctx, xi.mem)
     return LayerResult(out, MemoryAudit(au.peak, au.model))
 
 
@@ -333,6 +344,7 @@ def recombine_fragments(fragments, windows: Sequence[Sequence[int]], original_ba
     out = _out_like(fragments, (int(original_batch), f) + tuple(stride[a] * n[a] for a in range(3)))
     check(lib().vxg_recombine(ctx.handle, xi.mem, xi.ptr, S, f, i64s(n), i64s(flat), len(windows),
                               int(original_batch), _ptr_of(out)))
+    _finish(ctx, xi.mem)
     return out
 
 
@@ -362,6 +374,7 @@ def pruned_fft_forward(img, padded, ctx=None):
     xi = _Arg(img)
     out = _complex_out(img, (p[0] // 2 + 1, p[1], p[2]))
     check(lib().vxg_fft_pruned_forward(ctx.handle, xi.mem, xi.ptr, i64s(n), i64s(p), _ptr_of(out)))
+    _finish(ctx, xi.mem)
     return out
 
 
@@ -372,6 +385,7 @@ def pruned_fft_inverse(spec, padded, crop, ctx=None):
     xi = _Arg(spec, np.complex64)
     out = _out_like(spec, tuple(c))
     check(lib().vxg_fft_pruned_inverse(ctx.handle, xi.mem, xi.ptr, i64s(p), i64s(c), _ptr_of(out)))
+    _finish(ctx, xi.mem)
     return out
 
 
@@ -384,6 +398,7 @@ def batched_fft_forward(imgs, padded, ctx=None):
     xi = _Arg(imgs)
     out = _complex_out(imgs, (b, p[2] // 2 + 1, p[1], p[0]))
     check(lib().vxg_fft_batched_forward(ctx.handle, xi.mem, xi.ptr, b, i64s(n), i64s(p), _ptr_of(out)))
+    _finish(ctx, xi.mem)
     return out
 
 
@@ -395,6 +410,7 @@ def batched_fft_inverse(spec, padded, crop, ctx=None):
     xi = _Arg(spec, np.complex64)
     out = _out_like(spec, (b,) + tuple(c))
     check(lib().vxg_fft_batched_inverse(ctx.handle, xi.mem, xi.ptr, b, i64s(p), i64s(c), _ptr_of(out)))
+    _finish(ctx, xi.mem)
     return out
 
 
