@@ -250,39 +250,56 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    // NaN scan of the staged box (mpf_pool rejects NaN, layers.hpp:429): each
+    // staged element once, instead of per use in the window loop
+    for (int e = threadIdx.x; e < M2_BX * M2_BY * M2_BZ; e += 256) {
+      const float v = box[e];
+      saw_nan |= v != v;
+    }
     if (!live) continue;
     const int64_t s = plane / g.f;
     const int fm = int(plane % g.f);
-    float* dst0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.mz + (z >> 1);
+    const int64_t mstep = int64_t(g.my) * g.mz;  // one fragment x row
+    // fragment pointers for D row parity (x even / odd) and column parity
+    float* q0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.mz +
+                (z >> 1) + int64_t(x0 >> 1) * mstep;
+    float* qe0 = q0 + int64_t(0 + offy) * fstride;
+    float* qe1 = q0 + int64_t(1 + offy) * fstride;
+    float* qo0 = q0 + int64_t(4 + offy) * fstride;
+    float* qo1 = q0 + int64_t(5 + offy) * fstride;
     const float* col = box + ly * M2_BZ + 2 * lz;
-    float prev0 = 0.f, prev1 = 0.f;
-#pragma unroll 4
-    for (int xr = 0; xr <= x1; ++xr) {
+    // 2x2 (y, z) maxima of box row xr for columns z and z + 1, in the
+    // reference's scan order (first of equal elements wins)
+    auto rowmax = [&](int xr, float& m0, float& m1) {
       const float* rw = col + xr * (M2_BY * M2_BZ);
       const float2 a01 = *reinterpret_cast<const float2*>(rw);
       const float2 b01 = *reinterpret_cast<const float2*>(rw + M2_BZ);
       const float a2 = rw[2], b2 = rw[M2_BZ + 2];
-      saw_nan |= (a01.x != a01.x) | (a01.y != a01.y) | (a2 != a2) | (b01.x != b01.x) |
-                 (b01.y != b01.y) | (b2 != b2);
-      // column z: (y, z), (y, z+1), (y+1, z), (y+1, z+1) in scan order
-      float m0 = a01.x;
+      m0 = a01.x;
       m0 = a01.y > m0 ? a01.y : m0;
       m0 = b01.x > m0 ? b01.x : m0;
       m0 = b01.y > m0 ? b01.y : m0;
-      // column z+1
-      float m1 = a01.y;
+      m1 = a01.y;
       m1 = a2 > m1 ? a2 : m1;
       m1 = b01.y > m1 ? b01.y : m1;
       m1 = b2 > m1 ? b2 : m1;
-      if (xr > 0) {
-        const int xd = x0 + xr - 1;
-        const int64_t o = int64_t(xd >> 1) * g.my * g.mz;
-        const int ox = (xd & 1) * 4 + offy;
-        dst0[(ox + 0) * fstride + o] = m0 > prev0 ? m0 : prev0;
-        dst0[(ox + 1) * fstride + o] = m1 > prev1 ? m1 : prev1;
-      }
-      prev0 = m0;
-      prev1 = m1;
+    };
+    float p0, p1;
+    rowmax(0, p0, p1);
+#pragma unroll 2
+    for (int xr = 1; xr <= x1; xr += 2) {
+      float m0, m1;
+      rowmax(xr, m0, m1);  // D row x0 + xr - 1 (even)
+      *qe0 = m0 > p0 ? m0 : p0;
+      *qe1 = m1 > p1 ? m1 : p1;
+      if (xr + 1 > x1) break;
+      float n0, n1;
+      rowmax(xr + 1, n0, n1);  // D row x0 + xr (odd)
+      *qo0 = n0 > m0 ? n0 : m0;
+      *qo1 = n1 > m1 ? n1 : m1;
+      p0 = n0;
+      p1 = n1;
+      qe0 += mstep; qe1 += mstep; qo0 += mstep; qo1 += mstep;
     }
   }
   if (saw_nan) *nan_flag = 1;
