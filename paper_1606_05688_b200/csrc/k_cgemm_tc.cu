@@ -27,9 +27,11 @@
 //                 144 B) + one bulk copy of the W chunk (already tf32 hi/lo in
 //                 the UMMA layout, written once per layer by wsplit_kernel);
 //                 completion tracked on full[slot];
-//   warps 8-11    converters: split X into tf32 hi/lo in the canonical
-//                 K-major no-swizzle core-matrix layout, fence the async
-//                 proxy, arrive on ready[slot];
+//   warps 8-11    converters: split X into tf32 hi/lo and write it to
+//                 tensor memory (row = TMEM lane, 64 columns per slot), so
+//                 the MMAs take A from TMEM and read only W from shared
+//                 memory (A and B from shared memory made the K = 8 MMAs
+//                 shared-memory-bandwidth bound), arrive on ready[slot];
 //   warp 1        MMA issuer (one thread): 24 tcgen05.mma per chunk, commit to
 //                 empty[slot] (frees the slot) and, after a tile's last chunk,
 //                 to tmem_full;
@@ -55,8 +57,8 @@ struct TcCfg {
   static constexpr int B_CHUNK = 8 * B_MAT;        // pre-split W chunk (w, re/im, hi/lo)
   static constexpr int RAW_A = TC_M * RAW_ROW;
   static constexpr int OFF_W = RAW_A;
-  static constexpr int OFF_A = RAW_A + B_CHUNK;    // split X (8 matrices)
-  static constexpr int SLOT = OFF_A + 8 * A_MAT;
+  static constexpr int SLOT = RAW_A + B_CHUNK;     // (split X lives in TMEM)
+  static constexpr int ACOL = 4 * FO;              // TMEM column of A slot 0 (64 columns per slot)
   static constexpr int SMEM = TC_SLOTS * SLOT + 128;
 };
 
@@ -94,6 +96,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+// A operand from tensor memory (row = lane, K along columns): the MMA then
+// reads only B from shared memory
+__device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -261,6 +274,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
       mbar_wait(&full[s], uint32_t((g / TC_SLOTS) & 1));
       uint8_t* slot = smem + s * C::SLOT;
       const uint8_t* raw = slot + c * RAW_ROW;
+      // split X row c into tf32 hi/lo and write it to TMEM lane c: matrix
+      // (w, re/im, hi/lo) = columns ACOL + 64 s + 8 * ((w*2 + comp)*2 + h) + channel
+      uint32_t u[64];
 #pragma unroll
       for (int hk = 0; hk < 2; ++hk) {
         float4 v[4];
@@ -268,19 +284,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
         for (int kk = 0; kk < 4; ++kk) v[kk] = *reinterpret_cast<const float4*>(raw + (4 * hk + kk) * 16);
 #pragma unroll
         for (int wc = 0; wc < 4; ++wc) {
-          float h[4], l[4];
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const float x = wc == 0 ? v[kk].x : wc == 1 ? v[kk].y : wc == 2 ? v[kk].z : v[kk].w;
-            split_tf32(x, h[kk], l[kk]);
+            float h, l;
+            split_tf32(x, h, l);
+            u[(wc * 2 + 0) * 8 + 4 * hk + kk] = __float_as_uint(h);
+            u[(wc * 2 + 1) * 8 + 4 * hk + kk] = __float_as_uint(l);
           }
-          *reinterpret_cast<float4*>(slot + C::OFF_A + (wc * 2 + 0) * C::A_MAT + tile_off(c, hk)) =
-              make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(slot + C::OFF_A + (wc * 2 + 1) * C::A_MAT + tile_off(c, hk)) =
-              make_float4(l[0], l[1], l[2], l[3]);
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::);  // generic-proxy STS -> tensor core
+      const uint32_t ta = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::ACOL + 64 * s);
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {"
+          "%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+          "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,"
+          "%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,"
+          "%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};\n" ::"r"(ta),
+          "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
+          "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15]),
+          "r"(u[16]), "r"(u[17]), "r"(u[18]), "r"(u[19]), "r"(u[20]), "r"(u[21]), "r"(u[22]), "r"(u[23]),
+          "r"(u[24]), "r"(u[25]), "r"(u[26]), "r"(u[27]), "r"(u[28]), "r"(u[29]), "r"(u[30]), "r"(u[31]),
+          "r"(u[32]), "r"(u[33]), "r"(u[34]), "r"(u[35]), "r"(u[36]), "r"(u[37]), "r"(u[38]), "r"(u[39]),
+          "r"(u[40]), "r"(u[41]), "r"(u[42]), "r"(u[43]), "r"(u[44]), "r"(u[45]), "r"(u[46]), "r"(u[47]),
+          "r"(u[48]), "r"(u[49]), "r"(u[50]), "r"(u[51]), "r"(u[52]), "r"(u[53]), "r"(u[54]), "r"(u[55]),
+          "r"(u[56]), "r"(u[57]), "r"(u[58]), "r"(u[59]), "r"(u[60]), "r"(u[61]), "r"(u[62]), "r"(u[63]));
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::);
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&ready[s]);
     }
   } else if (warp == 1) {
@@ -294,25 +324,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
         mbar_wait(&ready[s], uint32_t((g / TC_SLOTS) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const uint32_t slot = smem_u32(smem + s * C::SLOT);
-        const uint32_t sa = slot + C::OFF_A, sb = slot + C::OFF_W;
+        const uint32_t sb = slot + C::OFF_W;
+        const uint32_t ta = tmem + uint32_t(C::ACOL + 64 * s);
         const uint32_t first = kc > 0 ? 1u : 0u;
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
           const uint32_t dr = tmem + w * 2 * FO, di = dr + FO;
-          auto am = [&](int cc, int h) { return umma_desc(sa + ((w * 2 + cc) * 2 + h) * C::A_MAT); };
+          auto am = [&](int cc, int h) { return ta + uint32_t(((w * 2 + cc) * 2 + h) * 8); };
           auto bm = [&](int cc, int h) { return umma_desc(sb + ((w * 2 + cc) * 2 + h) * C::B_MAT); };
-          mma_tf32(dr, am(0, 0), bm(0, 0), idesc_tf32<FO>(false), first);  // Dr += Xr Wr
-          mma_tf32(dr, am(0, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32(dr, am(0, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
-          mma_tf32(dr, am(1, 0), bm(1, 0), idesc_tf32<FO>(true), 1);       // Dr -= Xi Wi
-          mma_tf32(dr, am(1, 0), bm(1, 1), idesc_tf32<FO>(true), 1);
-          mma_tf32(dr, am(1, 1), bm(1, 0), idesc_tf32<FO>(true), 1);
-          mma_tf32(di, am(0, 0), bm(1, 0), idesc_tf32<FO>(false), first);  // Di += Xr Wi
-          mma_tf32(di, am(0, 0), bm(1, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32(di, am(0, 1), bm(1, 0), idesc_tf32<FO>(false), 1);
-          mma_tf32(di, am(1, 0), bm(0, 0), idesc_tf32<FO>(false), 1);      // Di += Xi Wr
-          mma_tf32(di, am(1, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32(di, am(1, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(dr, am(0, 0), bm(0, 0), idesc_tf32<FO>(false), first);  // Dr += Xr Wr
+          mma_tf32_ta(dr, am(0, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(dr, am(0, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(dr, am(1, 0), bm(1, 0), idesc_tf32<FO>(true), 1);       // Dr -= Xi Wi
+          mma_tf32_ta(dr, am(1, 0), bm(1, 1), idesc_tf32<FO>(true), 1);
+          mma_tf32_ta(dr, am(1, 1), bm(1, 0), idesc_tf32<FO>(true), 1);
+          mma_tf32_ta(di, am(0, 0), bm(1, 0), idesc_tf32<FO>(false), first);  // Di += Xr Wi
+          mma_tf32_ta(di, am(0, 0), bm(1, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(di, am(0, 1), bm(1, 0), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(di, am(1, 0), bm(0, 0), idesc_tf32<FO>(false), 1);      // Di += Xi Wr
+          mma_tf32_ta(di, am(1, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
+          mma_tf32_ta(di, am(1, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
         }
         umma_commit(&empty[s]);                       // slot reusable once these MMAs finish
         if (kc == nchunks - 1) umma_commit(tmem_full);  // tile accumulated

@@ -161,6 +161,23 @@ def test_conv_fft_every_tile_size_vs_oracle(oracle, ctx, variant):
         assert rel_error(got, want) <= 1e-4, (T, variant, rel_error(got, want))
 
 
+@pytest.mark.parametrize("fo", [32, 48, 64, 80])
+def test_conv_fft_tensor_core_map_counts(oracle, ctx, fo):
+    """Every output-map count the tcgen05 contraction instantiates (its TMEM
+    accumulator split differs per count), several m-blocks and chunks."""
+    import paper_1606_05688_b200 as v
+    S, f, k, T = 3, 24, (3, 3, 3), 16
+    n = (2 * (T - 2) + 2, 3 * (T - 2) + 2, T + 5)
+    rng = np.random.default_rng(fo)
+    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 27))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    want = oracle.conv(x, w, b, True)
+    p = v.ConvLayerParams(w, b, "relu")
+    got = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
+    assert rel_error(got, want) <= 1e-4, rel_error(got, want)
+
+
 def test_conv_fft_pair_kernel_matches_single(ctx):
     """The CTA-pair forward transform computes the same transform as the one-CTA
     kernel (T = 32, an 80 -> 80 layer: the bench's deep-layer shape).  The two

@@ -41,7 +41,8 @@ def main():
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--S", type=int, default=1)
     ap.add_argument("--net", default="n537")
-    ap.add_argument("--extent", type=int, default=714)
+    ap.add_argument("--extent", type=int, default=722)
+    ap.add_argument("--tune", action="store_true")
     a = ap.parse_args()
     ctx = v.Context(0)
     res = {}
@@ -83,12 +84,17 @@ def main():
         w = v.random_weights(net, 1)
         m = v.Model(net, w, ctx)
         e = a.extent
+        algos = None
+        if a.tune:
+            m.tune(1, e)
+            algos = ["direct"] + ["auto"] * (net.conv_count - 1)
+        plan = m.plan_info(1, e, algos)
         x = torch.rand((1, 1, e, e, e), device="cuda", generator=g) * 2 - 1
-        m.forward(x, cache_spectra=False)
+        m.forward(x, cache_spectra=False, conv_algos=algos)
         ctx.sync()
         ctx.profile(True)
         t0 = time.perf_counter()
-        _, rep = m.forward(x, cache_spectra=False)
+        _, rep = m.forward(x, cache_spectra=False, conv_algos=algos)
         ctx.sync()
         wall = time.perf_counter() - t0
         ks = ctx.kernel_stats()
@@ -96,6 +102,8 @@ def main():
         res["net_%s_%d" % (a.net, e)] = {
             "seconds": rep.seconds, "wall": wall,
             "layers": [round(s, 4) for s in rep.layer_seconds],
+            "planned": [round(l["seconds"], 4) for l in plan],
+            "plan": [(l.get("algo", "pool"), l.get("T", 0)) for l in plan],
             "kernels": {k: {"s": round(s["seconds"], 4), "n": s["launches"],
                             "TFLOPs": round(s["flops"] / s["seconds"] / 1e12, 1) if s["flops"] else None,
                             "GBps": round(s["bytes"] / s["seconds"] / 1e9) if s["bytes"] else None}
