@@ -53,6 +53,8 @@ struct GemmArgs {
   int mblocks, iblocks;
   int T;                     // tile size (for the algorithmic flop count)
   int64_t npairs;            // tensor-core path: frequency pairs
+  long long* prof = nullptr; // VXG_TC_PROF: per-CTA role cycle counters
+  int dbg = 0;               // VXG_TC_DBG experiment switches (results invalid when set)
 };
 
 extern const int kTileSizes[];

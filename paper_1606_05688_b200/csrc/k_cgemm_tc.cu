@@ -37,6 +37,10 @@
 //                 to tmem_full;
 //   warps 4-7     epilogue (TMEM lane quadrants 0-3): tcgen05.ld, 16-byte
 //                 stores of the Y pieces, arrive on tmem_empty.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "async.cuh"
 #include "common.cuh"
 #include "fftconv.hpp"
@@ -244,9 +248,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
   if (warp == 0) {
     // ---------------- producer ----------------
     const float4* xsrc = reinterpret_cast<const float4*>(a.X);  // one float4 = 2 complex
+    long long pw = 0;
     for (int64_t g = 0; g < nitems; ++g) {
       const int s = int(g % TC_SLOTS);
+      const long long t0 = a.prof ? clock64() : 0;
       if (g >= TC_SLOTS) mbar_wait(&empty[s], uint32_t((g / TC_SLOTS - 1) & 1));
+      if (a.prof) pw += clock64() - t0;
       const TileCoord tc = coord(g / nchunks);
       const int kc = int(g % nchunks);
       uint8_t* slot = smem + s * C::SLOT;
@@ -266,12 +273,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
       }
       cp_async_arrive_noinc(&full[s]);
     }
+    if (a.prof && lane == 0) a.prof[blockIdx.x * 8 + 0] = pw;
   } else if (warp >= 8) {
     // ---------------- converters: thread c owns row c ----------------
     const int c = tid - 256;
+    long long cw = 0, cb = 0;
     for (int64_t g = 0; g < nitems; ++g) {
       const int s = int(g % TC_SLOTS);
+      const long long t0 = a.prof ? clock64() : 0;
       mbar_wait(&full[s], uint32_t((g / TC_SLOTS) & 1));
+      const long long t1 = a.prof ? clock64() : 0;
+      cw += t1 - t0;
       uint8_t* slot = smem + s * C::SLOT;
       const uint8_t* raw = slot + c * RAW_ROW;
       // split X row c into tf32 hi/lo and write it to TMEM lane c: matrix
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
         }
       }
       const uint32_t ta = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::ACOL + 64 * s);
-      asm volatile(
+      if (!(a.dbg & 1)) asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {"
           "%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
           "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,"
@@ -312,41 +324,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&ready[s]);
+      if (a.prof) cb += clock64() - t1;
+    }
+    if (a.prof && c == 0) {
+      a.prof[blockIdx.x * 8 + 1] = cw;
+      a.prof[blockIdx.x * 8 + 2] = cb;
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
+      long long me = 0, mr = 0;
+      const long long tstart = a.prof ? clock64() : 0;
       for (int64_t g = 0; g < nitems; ++g) {
         const int s = int(g % TC_SLOTS);
         const int kc = int(g % nchunks);
         const int64_t t = g / nchunks;
+        const long long t0 = a.prof ? clock64() : 0;
         if (kc == 0 && t > 0) mbar_wait(tmem_empty, uint32_t((t - 1) & 1));  // epilogue drained TMEM
+        const long long t1 = a.prof ? clock64() : 0;
         mbar_wait(&ready[s], uint32_t((g / TC_SLOTS) & 1));
+        if (a.prof) {
+          me += t1 - t0;
+          mr += clock64() - t1;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const uint32_t slot = smem_u32(smem + s * C::SLOT);
         const uint32_t sb = slot + C::OFF_W;
         const uint32_t ta = tmem + uint32_t(C::ACOL + 64 * s);
         const uint32_t first = kc > 0 ? 1u : 0u;
+        // the four accumulators (w0 re, w0 im, w1 re, w1 im) round-robin, so
+        // consecutive MMAs never target the same accumulator
+        auto am = [&](int w, int cc, int h) { return ta + uint32_t(((w * 2 + cc) * 2 + h) * 8); };
+        auto bm = [&](int w, int cc, int h) { return umma_desc(sb + ((w * 2 + cc) * 2 + h) * C::B_MAT); };
+        const uint32_t ip = idesc_tf32<FO>(false), in = idesc_tf32<FO>(true);
+        // term list per accumulator: (A comp, A half, B comp, B half, negate)
+        constexpr int TR[6][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 1, 0}, {0, 1, 0, 0, 0},
+                                  {1, 0, 1, 0, 1}, {1, 0, 1, 1, 1}, {1, 1, 1, 0, 1}};  // Dr = XrWr - XiWi
+        constexpr int TI[6][5] = {{0, 0, 1, 0, 0}, {0, 0, 1, 1, 0}, {0, 1, 1, 0, 0},
+                                  {1, 0, 0, 0, 0}, {1, 0, 0, 1, 0}, {1, 1, 0, 0, 0}};  // Di = XrWi + XiWr
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          const uint32_t dr = tmem + w * 2 * FO, di = dr + FO;
-          auto am = [&](int cc, int h) { return ta + uint32_t(((w * 2 + cc) * 2 + h) * 8); };
-          auto bm = [&](int cc, int h) { return umma_desc(sb + ((w * 2 + cc) * 2 + h) * C::B_MAT); };
-          mma_tf32_ta(dr, am(0, 0), bm(0, 0), idesc_tf32<FO>(false), first);  // Dr += Xr Wr
-          mma_tf32_ta(dr, am(0, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32_ta(dr, am(0, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
-          mma_tf32_ta(dr, am(1, 0), bm(1, 0), idesc_tf32<FO>(true), 1);       // Dr -= Xi Wi
-          mma_tf32_ta(dr, am(1, 0), bm(1, 1), idesc_tf32<FO>(true), 1);
-          mma_tf32_ta(dr, am(1, 1), bm(1, 0), idesc_tf32<FO>(true), 1);
-          mma_tf32_ta(di, am(0, 0), bm(1, 0), idesc_tf32<FO>(false), first);  // Di += Xr Wi
-          mma_tf32_ta(di, am(0, 0), bm(1, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32_ta(di, am(0, 1), bm(1, 0), idesc_tf32<FO>(false), 1);
-          mma_tf32_ta(di, am(1, 0), bm(0, 0), idesc_tf32<FO>(false), 1);      // Di += Xi Wr
-          mma_tf32_ta(di, am(1, 0), bm(0, 1), idesc_tf32<FO>(false), 1);
-          mma_tf32_ta(di, am(1, 1), bm(0, 0), idesc_tf32<FO>(false), 1);
+        for (int k = 0; k < ((a.dbg & 4) ? 0 : 6); ++k) {
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const uint32_t dr = tmem + w * 2 * FO, di = dr + FO;
+            const uint32_t acc = k == 0 ? first : 1u;
+            mma_tf32_ta(dr, am(w, TR[k][0], TR[k][1]), bm(w, TR[k][2], TR[k][3]), TR[k][4] ? in : ip, acc);
+            mma_tf32_ta(di, am(w, TI[k][0], TI[k][1]), bm(w, TI[k][2], TI[k][3]), TI[k][4] ? in : ip, acc);
+          }
         }
         umma_commit(&empty[s]);                       // slot reusable once these MMAs finish
         if (kc == nchunks - 1) umma_commit(tmem_full);  // tile accumulated
+      }
+      if (a.prof) {
+        a.prof[blockIdx.x * 8 + 3] = me;
+        a.prof[blockIdx.x * 8 + 4] = mr;
+        a.prof[blockIdx.x * 8 + 7] = clock64() - tstart;
       }
     }
   } else if (warp >= 4) {
@@ -354,8 +386,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
     const int q = warp - 4;
     const int row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    long long ew = 0, eb = 0;
     for (int64_t t = 0; t < my_tiles; ++t) {
+      const long long t0 = a.prof ? clock64() : 0;
       mbar_wait(tmem_full, uint32_t(t & 1));
+      const long long t1 = a.prof ? clock64() : 0;
+      ew += t1 - t0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const TileCoord tc = coord(t);
       const int64_t m = tc.m0 + row;
@@ -376,7 +412,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
               : "r"(lane_base + col));
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-        if (m < a.M) {
+        if (m < a.M && !(a.dbg & 2)) {
 #pragma unroll
           for (int ii = 0; ii < 16; ++ii)
             yrow[(i0 + ii) * 8] = make_float4(__uint_as_float(v[0][ii]), __uint_as_float(v[1][ii]),
@@ -385,6 +421,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(tmem_empty);
+      if (a.prof) eb += clock64() - t1;
+    }
+    if (a.prof && q == 0 && lane == 0) {
+      a.prof[blockIdx.x * 8 + 5] = ew;
+      a.prof[blockIdx.x * 8 + 6] = eb;
     }
   }
   // warps 2-3 have no role
@@ -407,9 +448,33 @@ void tc_t(Ctx* c, GemmArgs a) {
   a.mblocks = int((a.M + TC_M - 1) / TC_M);
   const int64_t ntiles = int64_t(a.mblocks) * a.npairs;  // npairs = 8 per 16-frequency line
   const unsigned grid = unsigned(std::min<int64_t>(ntiles, c->num_sms));
+  // VXG_TC_PROF=1: per-role wait / busy cycles (clock64) printed per launch
+  static const bool prof = std::getenv("VXG_TC_PROF") != nullptr;
+  static const int dbg = std::getenv("VXG_TC_DBG") ? std::atoi(std::getenv("VXG_TC_DBG")) : 0;
+  a.dbg = dbg;
+  long long* dprof = nullptr;
+  if (prof) {
+    VXG_CUDA_CHECK(cudaMalloc(&dprof, size_t(grid) * 8 * sizeof(long long)));
+    VXG_CUDA_CHECK(cudaMemset(dprof, 0, size_t(grid) * 8 * sizeof(long long)));
+    a.prof = dprof;
+  }
   cgemm_tc_kernel<FO><<<grid, TC_THREADS, C::SMEM, c->stream>>>(a);
   c->counted();
   check_launch("cgemm_tc_kernel");
+  if (prof) {
+    std::vector<long long> h(size_t(grid) * 8);
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    VXG_CUDA_CHECK(cudaMemcpy(h.data(), dprof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(dprof);
+    double m[8] = {0};
+    for (unsigned b = 0; b < grid; ++b)
+      for (int k = 0; k < 8; ++k) m[k] += double(h[b * 8 + k]) / grid;
+    std::fprintf(stderr,
+                 "[tcprof] M=%lld total %.3gM | producer wait %.3gM | converter wait %.3gM busy %.3gM | "
+                 "mma wait-epilogue %.3gM wait-ready %.3gM | epilogue wait %.3gM busy %.3gM\n",
+                 (long long)a.M, m[7] / 1e6, m[0] / 1e6, m[1] / 1e6, m[2] / 1e6, m[3] / 1e6, m[4] / 1e6,
+                 m[5] / 1e6, m[6] / 1e6);
+  }
 }
 
 template <int FO>
