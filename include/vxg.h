@@ -212,6 +212,15 @@ int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S,
                       const int64_t e[3], const int* conv_algos, int cache_spectra,
                       float* dense_out, vxg_report* report);
 
+/* Streaming forward over `count` patches of the same shape (the tiler's
+ * production path): double-buffered device tensors and two copy streams, so
+ * the upload of patch k + 1 and the download of patch k - 1 overlap the
+ * forward of patch k (pinned host buffers give true overlap).  seconds
+ * (optional) = device time from the first upload to the last download. */
+int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* inputs, int64_t S,
+                           const int64_t e[3], const int* conv_algos, int cache_spectra,
+                           float* const* outputs, double* seconds);
+
 /* Measured-time planning: times the candidate tile sizes (and the direct
  * kernel where it may compete) for every conv layer of the plan of (S, e) on
  * sample inputs; later plans of this model choose per layer by measured cost. */

@@ -100,6 +100,8 @@ def lib() -> C.CDLL:
         "vxg_net_forward": (I, [P, P, P, I, P, I64, A, C.POINTER(I), P, C.POINTER(Report)]),
         "vxg_model_create": (I, [P, P, P, I, C.POINTER(P)]),
         "vxg_model_tune": (I, [P, I64, A]),
+        "vxg_model_forward_many": (I, [P, I64, C.POINTER(P), I64, A, C.POINTER(I), I, C.POINTER(P),
+                                       C.POINTER(C.c_double)]),
         "vxg_model_plan_info": (I, [P, I64, A, C.POINTER(I), A]),
         "vxg_model_free": (I, [P]),
         "vxg_model_forward": (I, [P, I, P, I64, A, C.POINTER(I), I, P, C.POINTER(Report)]),

@@ -697,6 +697,83 @@ int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S, 
   });
 }
 
+int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* inputs, int64_t S,
+                           const int64_t e_[3], const int* conv_algos, int cache_spectra,
+                           float* const* outputs, double* seconds) {
+  return guard([&] {
+    need(model, "vxg_model_forward_many: model");
+    require(count >= 0, "vxg_model_forward_many: count must be >= 0");
+    need(inputs, "vxg_model_forward_many: inputs");
+    need(outputs, "vxg_model_forward_many: outputs");
+    Model& m = *model->m;
+    Ctx* c = m.c;
+    const V3 e = v3_checked(e_, "vxg_model_forward_many: e");
+    const ForwardPlan p = m.plan(S, e, conv_algos);
+    const int64_t nin = S * m.net.fin * e.vol(), nout = S * p.f_out * p.dense.vol();
+    for (int64_t k = 0; k < count; ++k) {
+      need(inputs[k], "vxg_model_forward_many: input");
+      need(outputs[k], "vxg_model_forward_many: output");
+    }
+    AuditScope au(c);
+    // two copy streams (PCIe is full duplex) and double-buffered device tensors:
+    // patch k + 1 uploads and patch k - 1 downloads while patch k runs
+    struct Streams {
+      cudaStream_t in = nullptr, out = nullptr;
+      cudaEvent_t ev[8] = {};
+      ~Streams() {
+        for (auto& x : ev)
+          if (x) cudaEventDestroy(x);
+        if (in) cudaStreamDestroy(in);
+        if (out) cudaStreamDestroy(out);
+      }
+    } st;
+    VXG_CUDA_CHECK(cudaStreamCreateWithFlags(&st.in, cudaStreamNonBlocking));
+    VXG_CUDA_CHECK(cudaStreamCreateWithFlags(&st.out, cudaStreamNonBlocking));
+    for (auto& x : st.ev) VXG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    cudaEvent_t* h2d_done = st.ev;      // [2]
+    cudaEvent_t* fwd_done = st.ev + 2;  // [2]
+    cudaEvent_t* d2h_done = st.ev + 4;  // [2]
+    DevBuf din[2], dout[2];
+    for (int b = 0; b < 2 && b < count; ++b) {
+      din[b].alloc(c, nin * 4);
+      dout[b].alloc(c, nout * 4);
+    }
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // buffers exist before the copy streams use them
+    cudaEvent_t t0, t1;
+    VXG_CUDA_CHECK(cudaEventCreate(&t0));
+    VXG_CUDA_CHECK(cudaEventCreate(&t1));
+    VXG_CUDA_CHECK(cudaEventRecord(t0, c->stream));
+    VXG_CUDA_CHECK(cudaStreamWaitEvent(st.in, t0, 0));
+    auto h2d = [&](int64_t k) {
+      const int b = int(k & 1);
+      if (k >= 2) VXG_CUDA_CHECK(cudaStreamWaitEvent(st.in, fwd_done[b], 0));
+      VXG_CUDA_CHECK(cudaMemcpyAsync(din[b].get(), inputs[k], size_t(nin) * 4, cudaMemcpyHostToDevice, st.in));
+      VXG_CUDA_CHECK(cudaEventRecord(h2d_done[b], st.in));
+    };
+    if (count > 0) h2d(0);
+    for (int64_t k = 0; k < count; ++k) {
+      const int b = int(k & 1);
+      if (k + 1 < count) h2d(k + 1);
+      VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, h2d_done[b], 0));
+      if (k >= 2) VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, d2h_done[b], 0));
+      m.forward(p, din[b].as<float>(), dout[b].as<float>(), cache_spectra != 0, nullptr);
+      VXG_CUDA_CHECK(cudaEventRecord(fwd_done[b], c->stream));
+      VXG_CUDA_CHECK(cudaStreamWaitEvent(st.out, fwd_done[b], 0));
+      VXG_CUDA_CHECK(cudaMemcpyAsync(outputs[k], dout[b].get(), size_t(nout) * 4, cudaMemcpyDeviceToHost,
+                                     st.out));
+      VXG_CUDA_CHECK(cudaEventRecord(d2h_done[b], st.out));
+    }
+    VXG_CUDA_CHECK(cudaEventRecord(t1, st.out));
+    VXG_CUDA_CHECK(cudaEventSynchronize(t1));
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    VXG_CUDA_CHECK(cudaEventElapsedTime(&ms, t0, t1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (seconds) *seconds = ms * 1e-3;
+  });
+}
+
 int vxg_model_tune(vxg_model* model, int64_t S, const int64_t e[3]) {
   return guard([&] {
     need(model, "vxg_model_tune: model");

@@ -555,13 +555,15 @@ void Model::tune(int64_t S, V3 e) {
         best_fft = std::min(best_fft, kv.second.first + kv.second.second * double(q.tiles));
       }
       if (ch.algo == VXG_CONV_DIRECT || dmodel < 4.0 * best_fft) {
-        const V3 ns{40 + k.x - 1, 40 + k.y - 1, 40 + k.z - 1};
-        DevBuf x(c, f * ns.vol() * 4), y(c, fo * 40 * 40 * 40 * 4);
+        // a sample big enough to fill every SM several times over
+        const int64_t d = f <= 8 ? 128 : 64;
+        const V3 ns{d + k.x - 1, d + k.y - 1, d + k.z - 1};
+        DevBuf x(c, f * ns.vol() * 4), y(c, fo * d * d * d * 4);
         fill_sample(c, x.as<float>(), f * ns.vol(), 777u);
         const double t = time_on_stream(c, [&] {
           conv_direct_device(c, x.as<float>(), 1, f, ns, w, fo, k, b, l.relu, y.as<float>());
         }, 2);
-        lc.direct_vox = t / (40.0 * 40.0 * 40.0);
+        lc.direct_vox = t / double(d * d * d);
       }
     }
     if (trace_on()) {

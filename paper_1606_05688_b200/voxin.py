@@ -576,6 +576,31 @@ class Model:
         e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]
         return int(lib().vxg_model_plan_bytes(self._p, int(S), i64s(e), _algos(self.net, conv_algos)))
 
+    def forward_many(self, inputs, outputs=None, conv_algos=None, cache_spectra=True):
+        """Streaming forward over host patches of one shape (vxg_model_forward_many):
+        uploads / downloads overlap the forwards.  inputs: list of (S, f_in, *e)
+        float32 host arrays (pinned for true overlap); returns (outputs, seconds)."""
+        if not inputs:
+            return [], 0.0
+        S = int(inputs[0].shape[0])
+        e = [int(v) for v in inputs[0].shape[2:]]
+        shape = self.output_shape(S, e)
+        if outputs is None:
+            outputs = [np.empty(shape, np.float32) for _ in inputs]
+        for x in inputs:
+            if tuple(x.shape) != tuple(inputs[0].shape) or x.dtype != np.float32 or not x.flags.c_contiguous:
+                raise ValueError("forward_many: inputs must be C-contiguous float32 of one shape")
+        for y in outputs:
+            if tuple(y.shape) != shape or y.dtype != np.float32 or not y.flags.c_contiguous:
+                raise ValueError("forward_many: outputs must be C-contiguous float32 of the output shape")
+        ins = (C.c_void_p * len(inputs))(*[x.ctypes.data for x in inputs])
+        outs = (C.c_void_p * len(outputs))(*[y.ctypes.data for y in outputs])
+        sec = C.c_double()
+        check(lib().vxg_model_forward_many(self._p, len(inputs), ins, S, i64s(e),
+                                           _algos(self.net, conv_algos), 1 if cache_spectra else 0, outs,
+                                           C.byref(sec)))
+        return outputs, sec.value
+
     def tune(self, S: int, e):
         """Measured-time planning for input (S, f_in, e) (vxg_model_tune)."""
         e = [int(v) for v in (e if isinstance(e, (list, tuple)) else (e, e, e))]

@@ -73,6 +73,24 @@ def test_measured_planner_keeps_parity(golden, ctx, name):
     model.close()
 
 
+def test_forward_many_matches_single_forwards(ctx):
+    """The streaming API (double-buffered uploads / downloads on copy streams)
+    returns, patch for patch, exactly what single forwards return."""
+    import torch
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    w = v.random_weights(net, 5)
+    model = v.Model(net, w, ctx)
+    xs = [torch.from_numpy(v.fill_random((1, 1, 100, 100, 100), 20 + i)).pin_memory().numpy() for i in range(3)]
+    outs, sec = model.forward_many(xs)
+    assert sec > 0 and len(outs) == 3
+    for x, y in zip(xs, outs):
+        want, _ = model.forward(x)
+        assert np.array_equal(y, want)
+    model.close()
+
+
 def test_forward_independent_of_budget_and_algorithm(ctx):
     """Any feasible execution gives the same dense result (execute.hpp:384-386):
     fragment groups forced small by the budget reproduce the unconstrained run
