@@ -29,6 +29,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 NET = "n537"
+# smallest admissible cubic patch per bundled net: the CPU
+# reference runs there
+SMALLEST = {"n337": 92, "n537": 170, "n726": 120, "n926": 158}
 # ncu DRAM bytes per launch / the launch's algorithmic bytes (profiles/r1_ncu_summary.md):
 # cgemm_tc (M = 1728, in place): (22.89 + 19.35) GB / (2 x 19.26 GB X,Y + 1.78 GB W)
 TRAFFIC_RATIO = {"cgemm": round((22.89 + 19.35) / (2 * 19.26 + 1.78), 3)}
@@ -41,6 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--net", default=NET, choices=["n337", "n537", "n726", "n926"],
+                    help="bundled network (the headline metric is n537)")
     ap.add_argument("--extent", type=int, default=0, help="cubic input extent (0: largest that fits)")
     ap.add_argument("--budget-gb", type=float, default=0.0)
     ap.add_argument("--cache-spectra", type=int, default=0,
@@ -128,19 +133,19 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def pick_extent(model, budget_bytes, fov, hi=2048, stride=8, residue=2, algos=None):
-    """Largest admissible extent (e = residue mod stride) whose plan fits."""
+def pick_extent(model, budget_bytes, fov, hi=2048, algos=None, fout=3):
+    """Largest admissible extent (one that propagates through every MPF) whose plan fits."""
     best = None
-    e = hi - ((hi - residue) % stride)
+    e = hi
     while e >= fov:
         need = model.plan_bytes(1, e, algos)
         if 0 < need:
             # device input + dense output of the timed run live outside the plan
-            extra = 4 * (e ** 3) + 4 * 3 * (e - fov + 1) ** 3
+            extra = 4 * (e ** 3) + 4 * fout * (e - fov + 1) ** 3
             if need + extra <= budget_bytes:
                 best = e
                 break
-        e -= stride
+        e -= 1
     return best
 
 
@@ -184,34 +189,34 @@ def run_reference(args, ws, rank):
     from oracle.refbind import Ref
     from paper_1606_05688_b200.bundled_nets import FOV, NETS
     ref = Ref(workers=0)
-    e = 170  # smallest admissible n537 patch: the largest one the CPU path finishes in bounded time
+    e = SMALLEST[args.net]  # smallest admissible patch: what the CPU path finishes in bounded time
     # one forward is ~60 s on 16 host cores: at most 1 warm-up + 3 timed forwards
     # keep the arm within a few minutes (the counts actually run are reported)
     warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))
     times = []
     for i in range(warm + steps):
-        secs, spent, vox = ref.net_sample(NETS[NET], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
+        secs, spent, vox = ref.net_sample(NETS[args.net], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
         if i >= warm:
             times.append(secs)
     t = sum(times)
-    vox = (e - FOV[NET] + 1) ** 3
+    vox = (e - FOV[args.net] + 1) ** 3
     value = vox * len(times) / t
     line = {
-        "impl": "reference", "metric": f"output voxels/sec, {NET} sliding-window inference",
+        "impl": "reference", "metric": f"output voxels/sec, {args.net} sliding-window inference",
         "value": value, "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{NET} full forward, input {e}^3 -> dense 3x{e - FOV[NET] + 1}^3, "
+        "config": {"workload": f"{args.net} full forward, input {e}^3 -> dense {e - FOV[args.net] + 1}^3, "
                                "all pools MPF, reference host primitives (direct for f=1 layers, "
-                               "fft_task_parallel otherwise)", "net": NET, "extent": e},
+                               "fft_task_parallel otherwise)", "net": args.net, "extent": e},
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
-                         "sample": f"full {NET} forward at the smallest admissible patch {e}^3 per step"},
+                         "sample": f"full {args.net} forward at the smallest admissible patch {e}^3 per step"},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline():
+def cpu_baseline(args):
     """Reference CPU path on the box's host cores (rank 0, N = 1): one full n537
     forward at its smallest admissible patch through oracle/_ref."""
     try:
@@ -225,12 +230,12 @@ def cpu_baseline():
     except FileNotFoundError as ex:
         return {"value": None, "unit": "voxels/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {ex}"}
-    e = 170
-    secs, spent, vox = ref.net_sample(NETS[NET], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
+    e = SMALLEST[args.net]
+    secs, spent, vox = ref.net_sample(NETS[args.net], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
     return {"value": vox / secs, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
             "seconds": secs,
-            "sample": f"one full {NET} forward at its smallest admissible patch {e}^3 -> dense "
-                      f"{e - FOV[NET] + 1}^3 (oracle/_ref built from the unmodified reference; "
+            "sample": f"one full {args.net} forward at its smallest admissible patch {e}^3 -> dense "
+                      f"{e - FOV[args.net] + 1}^3 (oracle/_ref built from the unmodified reference; "
                       "direct conv for f=1 layers, fft_task_parallel otherwise; fp32)"}
 
 
@@ -251,8 +256,8 @@ def main():
     import paper_1606_05688_b200 as v
     from paper_1606_05688_b200.bundled_nets import FOV, NETS
 
-    net = v.parse_network_spec(NETS[NET])
-    fov = FOV[NET]
+    net = v.parse_network_spec(NETS[args.net])
+    fov = FOV[args.net]
     weights = v.random_weights(net, 1)
     peaks, peaks_src = measured_peaks()
 
@@ -261,6 +266,10 @@ def main():
     model = v.Model(net, weights, ctx)
     budget_bytes = ctx.memory()["budget"]
     nconv = sum(1 for l in net.layers if l[0] == "conv")
+    step = 1  # admissible extents repeat with the MPF stride product
+    for l in net.layers:
+        if l[0] == "pool":
+            step *= l[1][0]
 
     def choose(tuned):
         """(extent, conv algos): the largest fitting patch, or -- with measured
@@ -273,13 +282,13 @@ def main():
         if args.quick:
             return 258, None
         if not tuned:
-            return pick_extent(model, budget_bytes * 0.97, fov), None
+            return pick_extent(model, budget_bytes * 0.97, fov, fout=net.features_out), None
         best = None
         for algos in (None, ["direct"] + ["auto"] * (nconv - 1)):
-            emax = pick_extent(model, budget_bytes * 0.97, fov, algos=algos)
+            emax = pick_extent(model, budget_bytes * 0.97, fov, algos=algos, fout=net.features_out)
             if emax is None:
                 continue
-            for e in range(emax, max(fov, emax - 8 * 12) - 1, -8):
+            for e in range(emax, max(fov, emax - step * 12) - 1, -step):
                 est = sum(l["seconds"] for l in model.plan_info(1, e, algos))
                 score = (e - fov + 1) ** 3 / est if est > 0 else 0
                 if best is None or score > best[0]:
@@ -304,7 +313,8 @@ def main():
     x_host = v.fill_random((1, 1, e, e, e), bench_seed(1 + rank, e))
     x_pin = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pin.cuda()
-    out_dev = torch.empty((1, 3, dense, dense, dense), dtype=torch.float32, device="cuda")
+    fout = net.features_out
+    out_dev = torch.empty((1, fout, dense, dense, dense), dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(ctx.stream())
     cache = bool(args.cache_spectra)
 
@@ -350,7 +360,7 @@ def main():
     value = ws * args.steps * voxels / elapsed
 
     # ---- e2e through the public API, host buffers ----
-    out_host = torch.empty((1, 3, dense, dense, dense), dtype=torch.float32).pin_memory()
+    out_host = torch.empty((1, fout, dense, dense, dense), dtype=torch.float32).pin_memory()
     xin = x_pin.numpy()
     oh = out_host.numpy()
     model.forward(xin, out=oh, conv_algos=algos, cache_spectra=cache)  # warm
@@ -421,13 +431,13 @@ def main():
                               "whole-image pruned FFT and direct, P_fp32 = measured FFMA peak"}
 
     line = {
-        "metric": f"output voxels/sec, {NET} 3D ConvNet sliding-window inference",
+        "metric": f"output voxels/sec, {args.net} 3D ConvNet sliding-window inference",
         "value": value, "unit": "voxels/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{NET} full forward per GPU, input patch {e}^3 -> dense 3x{dense}^3 "
+        "config": {"workload": f"{args.net} full forward per GPU, input patch {e}^3 -> dense {net.features_out}x{dense}^3 "
                                "(largest admissible patch fitting the HBM budget)",
-                   "net": NET, "extent": e, "dense_out": dense, "global_batch": ws,
+                   "net": args.net, "extent": e, "dense_out": dense, "global_batch": ws,
                    "parallelism": f"independent halo patches x{ws}",
                    "kernel_spectra": "cached across steps" if cache else "recomputed every step",
                    "planner": ("modelled" if args.no_tune else
@@ -446,7 +456,7 @@ def main():
         "kernels": kernels,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     model.close()

@@ -138,6 +138,18 @@ struct Ctx {
   std::vector<cudaEvent_t> spare_events;
   Arena* arena = nullptr;  // set while a network forward runs (forward.cu)
 
+  // device bytes really obtainable now: free memory plus what the pool holds
+  // unused (other users of the GPU -- e.g. torch tensors allocated after the
+  // budget was set -- are not in the budget)
+  i64 device_free() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return budget;
+    unsigned long long reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return i64(fr) + i64(reserved) - i64(used);
+  }
+
   // bytes a new allocation can get: the largest arena block, else the budget left
   i64 avail() {
     std::lock_guard<std::mutex> lk(mu);

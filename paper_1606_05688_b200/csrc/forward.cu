@@ -421,7 +421,7 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
   // and remap). A big job gets everything the budget leaves.
   {
     Sched sched(*this, p);
-    const int64_t avail0 = c->avail();
+    const int64_t avail0 = std::min(c->avail(), c->device_free() - (int64_t(512) << 20));
     const int64_t in0 = sched.in_bytes(0, p.S);
     const int64_t top = sched.peak(0, 0, p.S, false) - in0;
     int64_t arena_bytes = int64_t(double(avail0) * 0.995);

@@ -74,17 +74,30 @@ def assign(tiles: Sequence[Tile], rank: int, world: int) -> list:
 
 
 def run_tiles(forward: Callable, volume, tiles: Iterable[Tile], out=None,
-              done: Optional[set] = None):
+              done: Optional[set] = None, forward_many: Optional[Callable] = None, batch: int = 4):
     """forward(crop (1, f, *in_extent)) -> (1, f_out, *out_extent) array.
     Writes each tile's owned region into `out` (dense, (1, f_out, *dense)) if
-    given; returns {tile index: owned block}.  Tiles in `done` are skipped."""
+    given; returns {tile index: owned block}.  Tiles in `done` are skipped.
+    forward_many(list of crops) -> list of results (optional): tiles of one
+    extent then run `batch` at a time through it, so uploads and downloads of
+    neighbouring tiles overlap the forwards."""
     blocks = {}
-    for t in tiles:
-        if done is not None and t.index in done:
-            continue
+    todo = [t for t in tiles if not (done is not None and t.index in done)]
+
+    def crop_of(t):
         sl = tuple(slice(t.in_origin[a], t.in_origin[a] + t.in_extent[a]) for a in range(3))
-        crop = np.ascontiguousarray(volume[(slice(None), slice(None)) + sl])
-        res = np.asarray(forward(crop))
+        return np.ascontiguousarray(volume[(slice(None), slice(None)) + sl], dtype=np.float32)
+
+    results = {}
+    if forward_many is not None:
+        for b0 in range(0, len(todo), batch):
+            grp = todo[b0:b0 + batch]
+            same = all(t.in_extent == grp[0].in_extent for t in grp)
+            outs = forward_many([crop_of(t) for t in grp]) if same else [forward(crop_of(t)) for t in grp]
+            for t, r in zip(grp, outs):
+                results[t.index] = r
+    for t in todo:
+        res = np.asarray(results.pop(t.index)) if t.index in results else np.asarray(forward(crop_of(t)))
         rel = tuple(slice(t.write_origin[a] - t.out_origin[a],
                           t.write_origin[a] - t.out_origin[a] + t.write_extent[a]) for a in range(3))
         block = res[(slice(None), slice(None)) + rel]
@@ -144,7 +157,12 @@ def infer_volume(model, volume, tile_out, rank: int = 0, world: int = 1, gather:
         res, _ = model.forward(np.ascontiguousarray(crop, np.float32))
         return res
 
-    blocks = run_tiles(fwd, volume, mine, out if world == 1 else None, done)
+    def fwd_many(crops):
+        res, _ = model.forward_many(crops)
+        return res
+
+    blocks = run_tiles(fwd, volume, mine, out if world == 1 else None, done,
+                       forward_many=fwd_many if hasattr(model, "forward_many") else None)
     if world > 1 and gather:
         gather_to_root(blocks, tiles, out, model.net.features_out,
                        device="cuda" if _cuda_dist() else "cpu")

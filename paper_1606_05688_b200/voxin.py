@@ -172,6 +172,13 @@ def _is_torch_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
 
 
+def _torch_ready(x):
+    """The library runs on its own stream: torch work that produced (or last
+    used the memory of) a CUDA tensor must be complete before it is handed over."""
+    import torch
+    torch.cuda.current_stream(x.device).synchronize()
+
+
 class _Arg:
     """Resolves one tensor argument to (mem, pointer)."""
 
@@ -180,6 +187,7 @@ class _Arg:
             import torch
             if x.dtype != torch.float32 or not x.is_contiguous():
                 raise ValueError("device tensors must be contiguous float32")
+            _torch_ready(x)
             self.mem, self.ptr, self.keep = L.MEM_DEVICE, C.c_void_p(x.data_ptr()), x
         else:
             a = np.ascontiguousarray(x, dtype=dtype)
@@ -196,6 +204,7 @@ def _out_like(ref, shape, dtype=np.float32):
 
 def _ptr_of(t):
     if _is_torch_cuda(t):
+        _torch_ready(t)
         return C.c_void_p(t.data_ptr())
     return t.ctypes.data_as(C.c_void_p)
 

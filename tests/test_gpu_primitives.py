@@ -81,6 +81,37 @@ def test_recombine_bit_exact(golden, ctx):
         v.recombine_fragments(t, [(2, 2, 2)], 3, ctx)
 
 
+@pytest.mark.parametrize("wins,n", [([(2, 2, 2), (2, 2, 2)], (151, 150, 149)),
+                                    ([(2, 2, 2)] * 3, (75, 74, 76)),
+                                    ([(3, 2, 1), (1, 2, 3)], (60, 61, 62))])
+def test_recombine_large_vs_numpy(ctx, wins, n):
+    """Large fragment tensors (the bench's recombine sizes) against a numpy
+    restatement of recombine_fragments (layers.hpp:477-520)."""
+    import torch
+    import paper_1606_05688_b200 as v
+    alpha = int(np.prod([np.prod(w) for w in wins]))
+    S0, f = 2, 3
+    rng = np.random.default_rng(len(wins))
+    frag = rng.standard_normal((S0 * alpha, f) + n).astype(np.float32)
+    got = v.recombine_fragments(torch.from_numpy(frag).cuda(), wins, S0, ctx).cpu().numpy()
+    stride = [int(np.prod([w[a] for w in wins])) for a in range(3)]
+    want = np.empty((S0, f) + tuple(stride[a] * n[a] for a in range(3)), np.float32)
+    # fragment index: first pool's offset slowest; offset along axis a adds o * (stride before pool)
+    for s in range(S0):
+        for b in range(alpha):
+            rem, off = b, [0, 0, 0]
+            for wi in range(len(wins)):
+                vol = int(np.prod([np.prod(w) for w in wins[wi + 1:]])) if wi + 1 < len(wins) else 1
+                idx, rem = divmod(rem, vol)
+                w = wins[wi]
+                o = (idx // (w[1] * w[2]), (idx // w[2]) % w[1], idx % w[2])
+                pre = [int(np.prod([ww[a] for ww in wins[:wi]])) for a in range(3)]
+                for a in range(3):
+                    off[a] += o[a] * pre[a]
+            want[s, :, off[0]::stride[0], off[1]::stride[1], off[2]::stride[2]] = frag[s * alpha + b]
+    assert np.array_equal(got, want)
+
+
 def test_mpf_then_recombine_is_dense_max_filter(ctx):
     """layers_test.cpp:134-158: MPF + recombination == dense max filter, exactly."""
     import paper_1606_05688_b200 as v
