@@ -733,8 +733,14 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
     cudaEvent_t* h2d_done = st.ev;      // [2]
     cudaEvent_t* fwd_done = st.ev + 2;  // [2]
     cudaEvent_t* d2h_done = st.ev + 4;  // [2]
+    // double buffering only if the forward still fits next to the second pair
+    // of patch buffers (plan_bytes counts one input and one output)
+    const int64_t one = (nin + nout) * 4;
+    const int64_t need = m.plan_bytes(p, cache_spectra != 0, 0);
+    const int64_t room = std::min(c->avail(), c->device_free() - (int64_t(512) << 20));
+    const int nbuf = (count > 1 && need + one <= room) ? 2 : 1;
     DevBuf din[2], dout[2];
-    for (int b = 0; b < 2 && b < count; ++b) {
+    for (int b = 0; b < nbuf && b < count; ++b) {
       din[b].alloc(c, nin * 4);
       dout[b].alloc(c, nout * 4);
     }
@@ -745,23 +751,24 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
     VXG_CUDA_CHECK(cudaEventRecord(t0, c->stream));
     VXG_CUDA_CHECK(cudaStreamWaitEvent(st.in, t0, 0));
     auto h2d = [&](int64_t k) {
-      const int b = int(k & 1);
-      if (k >= 2) VXG_CUDA_CHECK(cudaStreamWaitEvent(st.in, fwd_done[b], 0));
+      const int b = int(k % nbuf);
+      if (k >= nbuf) VXG_CUDA_CHECK(cudaStreamWaitEvent(st.in, fwd_done[b], 0));
       VXG_CUDA_CHECK(cudaMemcpyAsync(din[b].get(), inputs[k], size_t(nin) * 4, cudaMemcpyHostToDevice, st.in));
       VXG_CUDA_CHECK(cudaEventRecord(h2d_done[b], st.in));
     };
     if (count > 0) h2d(0);
     for (int64_t k = 0; k < count; ++k) {
-      const int b = int(k & 1);
-      if (k + 1 < count) h2d(k + 1);
+      const int b = int(k % nbuf);
+      if (nbuf == 2 && k + 1 < count) h2d(k + 1);  // prefetch under this forward
       VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, h2d_done[b], 0));
-      if (k >= 2) VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, d2h_done[b], 0));
+      if (k >= nbuf) VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, d2h_done[b], 0));
       m.forward(p, din[b].as<float>(), dout[b].as<float>(), cache_spectra != 0, nullptr);
       VXG_CUDA_CHECK(cudaEventRecord(fwd_done[b], c->stream));
       VXG_CUDA_CHECK(cudaStreamWaitEvent(st.out, fwd_done[b], 0));
       VXG_CUDA_CHECK(cudaMemcpyAsync(outputs[k], dout[b].get(), size_t(nout) * 4, cudaMemcpyDeviceToHost,
                                      st.out));
       VXG_CUDA_CHECK(cudaEventRecord(d2h_done[b], st.out));
+      if (nbuf == 1 && k + 1 < count) h2d(k + 1);  // single buffer: after this forward read it
     }
     VXG_CUDA_CHECK(cudaEventRecord(t1, st.out));
     VXG_CUDA_CHECK(cudaEventSynchronize(t1));
