@@ -202,7 +202,7 @@ def run_reference(args, ws, rank):
     vox = (e - FOV[args.net] + 1) ** 3
     value = vox * len(times) / t
     line = {
-        "impl": "reference", "metric": f"output voxels/sec, {args.net} sliding-window inference",
+        "impl": "reference", "metric": f"output voxels/sec, {args.net} 3D ConvNet sliding-window inference",
         "value": value, "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
