@@ -16,6 +16,13 @@ namespace vxg {
 namespace {
 
 // VXG_NO_TC=1 pins the fp32 FFMA contraction (parity cross-checks, A/B timing)
+// VXG_YPAIR=1: pair-major Y (whole-line epilogue stores, TMA-gathered inverse).
+// Measured at T = 32: contraction -33 %, inverse +110 % -> off by default.
+bool ypair_enabled() {
+  const char* e = std::getenv("VXG_YPAIR");
+  return e && std::strcmp(e, "1") == 0;
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("VXG_NO_TC");
   return e && std::strcmp(e, "0") != 0;
@@ -41,7 +48,7 @@ int64_t fft_reserved_rows() {
 }
 
 int64_t fft_chunk_bytes(const FftPlan& plan, int64_t f, int64_t fo, int64_t rows) {
-  return rows * (plan.inplace ? f : f + fo) * plan.nwp * 8;
+  return rows * (f + fo) * plan.nwp * 8;
 }
 
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
@@ -71,7 +78,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tc = tc;
     p.pair = (T == 32 || T == 24) && tile_pair_enabled();  // measured wins (other T: one CTA is as fast)
     p.inv_pair = (T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled();  // measured wins
-    p.inplace = tc && f == fo;
+    p.ylw = (tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
     p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);
     const double nw = double(T) * T * (T / 2 + 1);
@@ -96,7 +103,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   p.pair = pair && T >= 24;  // tests: every pair-capable size
   p.inv_pair = pair && T >= 24;  // tests: every pair-capable size
   p.lw = 16;
-  p.inplace = p.tc && f == fo;
+  p.ylw = (p.tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
   p.nwp = tile_nwp(T, p.lw);
   return p;
 }
@@ -158,8 +165,8 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
                  (long long)M, (long long)rows, int(plan.tc));
   DevBuf X(c, rows * f * plan.nwp * 8);
   DevBuf Ybuf;
-  if (!plan.inplace) Ybuf.alloc(c, rows * fo * plan.nwp * 8);
-  const DevBuf& Y = plan.inplace ? X : Ybuf;
+  Ybuf.alloc(c, rows * fo * plan.nwp * 8);
+  const DevBuf& Y = Ybuf;
 
   for (int64_t m0 = 0; m0 < M; m0 += rows) {
     const int64_t mc = std::min(rows, M - m0);
@@ -188,6 +195,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ga.f = int(f);
     ga.fo = int(fo);
     ga.T = T;
+    ga.ypair = plan.ylw == 2 ? 1 : 0;
     if (plan.tc)
       launch_cgemm_tc(c, ga, plan.nwp / 2);
     else
@@ -207,7 +215,8 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ia.m0 = m0;
     ia.bias = bias;
     ia.relu = relu ? 1 : 0;
-    ia.lw = plan.lw;
+    ia.lw = plan.ylw;
+    ia.nwp = plan.nwp;
     ia.pair = plan.inv_pair;
     launch_tile_inv(c, T, ia, mc * fo);
   }

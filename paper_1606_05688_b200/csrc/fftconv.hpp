@@ -41,6 +41,7 @@ struct InvTileArgs {
   int relu;
   int lw = 16;
   bool pair = false;         // CTA-pair transform (tile_inv_pair_kernel)
+  int64_t nwp = 0;           // frequencies per (row, map) in the spectrum buffer
 };
 
 struct GemmArgs {
@@ -55,6 +56,7 @@ struct GemmArgs {
   int64_t npairs;            // tensor-core path: frequency pairs
   long long* prof = nullptr; // VXG_TC_PROF: per-CTA role cycle counters
   int dbg = 0;               // VXG_TC_DBG experiment switches (results invalid when set)
+  int ypair = 0;             // Y pair-major ([w/2][row][map][2]) instead of line-major
 };
 
 extern const int kTileSizes[];
@@ -81,12 +83,12 @@ struct FftPlan {
   V3 v;        // valid outputs per tile per axis
   V3 nt;       // tiles per axis
   int64_t tiles = 0;
-  int lw = 16;       // spectrum chunk width (frequencies per 128-byte line)
+  int lw = 16;       // X spectrum chunk width (frequencies per 128-byte line)
+  int ylw = 16;      // Y chunk width: 2 = pair-major (tcgen05 epilogue writes whole lines,
+                     // the CTA-pair inverse gathers its x lines by TMA)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
   bool pair = false;     // forward tile transform on a CTA pair (T >= 24)
   bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
-  bool inplace = false;  // tc with f == fo: Y overwrites X (each CTA tile reads
-                         // exactly the bytes it later writes, see k_cgemm_tc.cu)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };

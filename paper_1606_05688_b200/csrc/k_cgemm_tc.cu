@@ -16,9 +16,9 @@
 // fastest: the 8 CTAs reading pieces of the same lines run concurrently and
 // share them through L2.
 //
-// With f == fo, Y may alias X (plan.inplace): a tile's Y pieces are exactly
-// the bytes its X chunks were read from, no other CTA touches them, and the
-// epilogue writes only after the tile's last MMA (hence every read) completed.
+// Y is written line-major (16-byte pieces, like X) or, for the CTA-pair
+// inverse transform, pair-major ([w/2][row][map][2]): then a warp-local
+// transpose turns the epilogue's stores into whole-line writes.
 //
 // Persistent, warp-specialised pipeline over a flat stream of (tile, K-chunk)
 // items and a 3-slot shared-memory ring (raw X chunk | pre-split W chunk |
@@ -63,7 +63,8 @@ struct TcCfg {
   static constexpr int OFF_W = RAW_A;
   static constexpr int SLOT = RAW_A + B_CHUNK;     // (split X lives in TMEM)
   static constexpr int ACOL = 4 * FO;              // TMEM column of A slot 0 (64 columns per slot)
-  static constexpr int SMEM = TC_SLOTS * SLOT + 128;
+  static constexpr int STAGE = 4 * 4096;  // pair-major epilogue: 4 KB transpose tile per warp
+  static constexpr int SMEM = TC_SLOTS * SLOT + STAGE + 128;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -200,7 +201,8 @@ template <int FO>
 __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
   using C = TcCfg<FO>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_SLOTS * C::SLOT);
+  uint8_t* ystage = smem + TC_SLOTS * C::SLOT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_SLOTS * C::SLOT + C::STAGE);
   uint64_t* ready = full + TC_SLOTS;
   uint64_t* empty = ready + TC_SLOTS;
   uint64_t* tmem_full = empty + TC_SLOTS;
@@ -395,6 +397,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const TileCoord tc = coord(t);
       const int64_t m = tc.m0 + row;
+      if (a.ypair) {
+        // pair-major Y ([pair][row][map] 16-byte pieces): a row's maps are
+        // contiguous, so a warp-local transpose through shared memory (16-byte
+        // chunks XOR-swizzled by row) lets every store instruction write four
+        // whole 128-byte lines instead of 32 scattered pieces
+        uint8_t* stg = ystage + q * 4096;
+        float4* ybase = reinterpret_cast<float4*>(a.Y) + (tc.pair * a.mstride + tc.m0) * a.fo;
+#pragma unroll 1
+        for (int i0 = 0; i0 < FO; i0 += 8) {
+          uint32_t v[4][8];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t col = (qq >> 1) * 2 * FO + (qq & 1) * FO + i0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                : "=r"(v[qq][0]), "=r"(v[qq][1]), "=r"(v[qq][2]), "=r"(v[qq][3]), "=r"(v[qq][4]),
+                  "=r"(v[qq][5]), "=r"(v[qq][6]), "=r"(v[qq][7])
+                : "r"(lane_base + col));
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc)
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((cc ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(v[0][cc]), __uint_as_float(v[1][cc]), __uint_as_float(v[2][cc]),
+                            __uint_as_float(v[3][cc]));
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int r = 4 * k + (lane >> 3), cc = lane & 7;
+            const float4 piece = *reinterpret_cast<const float4*>(stg + r * 128 + ((cc ^ (r & 7)) << 4));
+            if (tc.m0 + q * 32 + r < a.M && !(a.dbg & 2)) ybase[int64_t(q * 32 + r) * a.fo + i0 + cc] = piece;
+          }
+          __syncwarp();
+        }
+      } else {
       float4* yrow = reinterpret_cast<float4*>(a.Y) + (tc.wb * a.mstride + m) * a.fo * 8 + tc.pip;
 #pragma unroll 1
       for (int i0 = 0; i0 < FO; i0 += 16) {
@@ -418,6 +455,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
             yrow[(i0 + ii) * 8] = make_float4(__uint_as_float(v[0][ii]), __uint_as_float(v[1][ii]),
                                               __uint_as_float(v[2][ii]), __uint_as_float(v[3][ii]));
         }
+      }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(tmem_empty);

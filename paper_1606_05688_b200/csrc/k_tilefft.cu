@@ -27,6 +27,9 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "async.cuh"
 #include "common.cuh"
 #include "fft_reg.cuh"
@@ -48,6 +51,30 @@ void init_twiddles() {
 }
 
 namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                           const uint64_t* strides, const uint32_t* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    VXG_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc),
+                                           cudaEnableDefault, &q));
+    if (!enc) throw cuda_failure("cuTensorMapEncodeTiled unavailable");
+  }
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], es[5];
+  for (int k = 0; k < rank; ++k) {
+    d[k] = dims[k];
+    bx[k] = box[k];
+    es[k] = 1;
+    if (k < rank - 1) st[k] = strides[k];
+  }
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<void*>(base), d, st,
+                         bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_failure("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
 
 template <int T>
 struct TileCfg {
@@ -220,6 +247,10 @@ struct PairCfg {
   static constexpr int HP = T / 2;                              // planes per CTA
   static constexpr int SMEM = HP * C::SX * 8;
   static constexpr int WORK = HP * C::H > HP * HP ? HP * C::H : HP * HP;
+  // inverse with a pair-major spectrum: per kx one TMA box of the CTA's ky
+  // half (HP*H complex), slabs padded to 128 bytes, staged in the plane buffer
+  static constexpr int SL = ((HP * C::H * 8 + 127) / 128) * 128 / 8;
+  static constexpr int SMEM_INV = (T * SL * 8 > SMEM ? T * SL * 8 : SMEM) + 16;
   static constexpr int THREADS = ((WORK + 31) / 32) * 32;
 };
 
@@ -539,7 +570,8 @@ __device__ __forceinline__ void st_peer(uint32_t addr, float2 v) {
 }
 
 template <int T>
-__global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvTileArgs a) {
+__global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvTileArgs a,
+                                                                           const __grid_constant__ CUtensorMap ymap) {
   using C = TileCfg<T>;
   using P = PairCfg<T>;
   constexpr int HP = P::HP;
@@ -558,13 +590,45 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
   const int x0 = int(r) * HP;  // my planes [x0, x0 + HP)
 
   // A+B: x lines (ky in my half, all kz) from HBM, inverse transform, scatter
+  float2 v[T];
+  const bool tma = a.lw == 2;
+  if (tma) {
+    // pair-major spectrum: the copy engine gathers the 16-byte pieces of my
+    // x lines (one box per kx) into the plane buffer, used as staging
+    uint64_t& bar = *reinterpret_cast<uint64_t*>(spf + 2 * ((P::SMEM_INV - 16) / 8));
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(T * HP * C::H * 8));
+      for (int kx = 0; kx < T; ++kx) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sp + kx * P::SL));
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(d),
+            "l"(&ymap), "r"(0), "r"(int(i)), "r"(int(ml)), "r"((kx * T * C::H + x0 * C::H) / 2), "r"(b)
+            : "memory");
+      }
+    }
+    __syncthreads();
+    asm volatile(
+        "{\n\t.reg .pred P;\nWTI_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t@!P bra WTI_%=;\n\t}\n" ::"r"(b)
+        : "memory");
+    if (tid < HP * C::H) {
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) v[kx] = sp[kx * P::SL + tid];
+    }
+    // both CTAs have read their staging before either scatters into the other
+    cluster_arrive();
+    cluster_wait();
+  }
   if (tid < HP * C::H) {
     const int lw = a.lw, lshift = __ffs(lw) - 1;
     const float2* src = a.spec + (ml * a.fo + i) * lw;
     const int64_t wb_stride = a.mstride * a.fo * lw;
     const int t0 = x0 * C::H + tid;  // ky * H + kz, ky = x0 + tid / H
-    float2 v[T];
-    if ((T * C::H) % 16 == 0 && lw == 16) {
+    if (tma) {
+    } else if ((T * C::H) % 16 == 0 && lw == 16) {
       const float2* g = src + int64_t(t0 >> 4) * wb_stride + (t0 & 15);
       const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
 #pragma unroll
@@ -727,13 +791,21 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
     static bool pconf = false;
     if (!pconf) {
       VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_pair_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM_INV));
       pconf = true;
+    }
+    CUtensorMap ymap{};
+    if (a.lw == 2) {
+      // pair-major Y: {4 floats of a pair, fo maps, mstride rows, pairs}
+      const uint64_t dims[4] = {4, uint64_t(a.fo), uint64_t(a.mstride), uint64_t(a.nwp) / 2};
+      const uint64_t strides[3] = {16, uint64_t(a.fo) * 16, uint64_t(a.mstride) * a.fo * 16};
+      const uint32_t box[4] = {4, 1, 1, uint32_t(P::HP * TileCfg<T>::H / 2)};
+      encode_tensor_map_f32(&ymap, a.spec, 4, dims, strides, box);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(2 * nblocks));
     cfg.blockDim = dim3(P::THREADS);
-    cfg.dynamicSmemBytes = P::SMEM;
+    cfg.dynamicSmemBytes = P::SMEM_INV;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -742,7 +814,7 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair_kernel<T>, a));
+    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair_kernel<T>, a, ymap));
     c->counted();
     check_launch("tile_inv_pair_kernel");
     return;

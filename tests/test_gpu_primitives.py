@@ -209,6 +209,23 @@ def test_conv_fft_tensor_core_map_counts(oracle, ctx, fo):
     assert rel_error(got, want) <= 1e-4, rel_error(got, want)
 
 
+def test_conv_fft_pair_major_spectrum_path(oracle, ctx, monkeypatch):
+    """The optional pair-major Y layout (VXG_YPAIR=1: transposing tcgen05
+    epilogue + TMA-gathered CTA-pair inverse) against the C oracle."""
+    import paper_1606_05688_b200 as v
+    monkeypatch.setenv("VXG_YPAIR", "1")
+    S, f, fo = 2, 16, 32
+    rng = np.random.default_rng(5)
+    for T in (24, 32):
+        k = (3, 4, 5)
+        n = (T + 9, 2 * T - 3, T + 4)
+        x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+        w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 60))).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+        got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, ctx=ctx)
+        assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4, T
+
+
 def test_conv_fft_pair_kernel_matches_single(ctx):
     """The CTA-pair forward transform computes the same transform as the one-CTA
     kernel (T = 32, an 80 -> 80 layer: the bench's deep-layer shape).  The two
