@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <string>
 #include <map>
 #include <tuple>
 
@@ -503,8 +504,46 @@ void fill_sample(Ctx* c, float* x, int64_t n, uint32_t seed) {
 // recorded as seconds per row; the direct kernel is timed too where the
 // model's estimate is within 4x of the FFT's.  plan() then scales the
 // per-row costs by each candidate's row count for the real extent.
+// Measured costs can be saved (VXG_TUNE_SAVE=<file>) and replayed
+// (VXG_TUNE_FILE=<file>) so that a profiled run (under ncu every launch is
+// serialised and timings are meaningless) executes the plan of a normal run.
+// One line per conv layer: "conv f fo kx ky kz direct_vox pool_elem {T fixed per_row}".
+namespace {
+std::string tune_key(int64_t f, int64_t fo, V3 k) {
+  return std::to_string(f) + " " + std::to_string(fo) + " " + std::to_string(k.x) + " " +
+         std::to_string(k.y) + " " + std::to_string(k.z);
+}
+}  // namespace
+
 void Model::tune(int64_t S, V3 e) {
   const ForwardPlan p0 = plan(S, e, nullptr);
+  std::map<std::string, LayerCosts> replay;
+  double replay_pool = -1;
+  if (const char* fn = std::getenv("VXG_TUNE_FILE")) {
+    if (FILE* fp = std::fopen(fn, "r")) {
+      char line[4096];
+      while (std::fgets(line, sizeof(line), fp)) {
+        long long f, fo, kx, ky, kz;
+        double dv, pe;
+        int off = 0;
+        if (std::sscanf(line, "conv %lld %lld %lld %lld %lld %lf %lf%n", &f, &fo, &kx, &ky, &kz, &dv, &pe,
+                        &off) != 7)
+          continue;
+        LayerCosts lc;
+        lc.direct_vox = dv;
+        replay_pool = pe;
+        const char* q = line + off;
+        int T, n = 0;
+        double a0, a1;
+        while (std::sscanf(q, "%d %lf %lf%n", &T, &a0, &a1, &n) == 3) {
+          lc.fft[T] = {a0, a1};
+          q += n;
+        }
+        replay[tune_key(f, fo, V3{kx, ky, kz})] = lc;
+      }
+      std::fclose(fp);
+    }
+  }
   for (size_t li = 0; li < net.layers.size(); ++li) {
     const Layer& l = net.layers[li];
     if (l.kind != 0) continue;
@@ -513,6 +552,12 @@ void Model::tune(int64_t S, V3 e) {
     const Shape& in = p0.shapes[li];
     const int64_t f = in.f, fo = l.fo;
     const V3 k = l.ext;
+    auto rit = replay.find(tune_key(f, fo, k));
+    if (rit != replay.end()) {
+      measured[ci] = rit->second;
+      if (replay_pool > 0) pool_elem = replay_pool;
+      continue;
+    }
     LayerCosts lc;
     const float* w = kern[size_t(ci)].as<float>();
     const float* b = bias[size_t(ci)].as<float>();
@@ -584,6 +629,21 @@ void Model::tune(int64_t S, V3 e) {
     fill_sample(c, x.as<float>(), f * nv.vol(), 99u);
     const double t = time_on_stream(c, [&] { launch_mpf(c, x.as<float>(), 1, f, nv, pw, y.as<float>()); }, 2);
     pool_elem = t / double(f * nv.vol());
+  }
+  if (const char* fn = std::getenv("VXG_TUNE_SAVE")) {
+    if (FILE* fp = std::fopen(fn, "w")) {
+      int64_t f = net.fin;
+      for (size_t li = 0; li < net.layers.size(); ++li) {
+        const Layer& l = net.layers[li];
+        if (l.kind != 0) continue;
+        const LayerCosts& lc = measured[conv_index[li]];
+        std::fprintf(fp, "conv %s %.6e %.6e", tune_key(f, l.fo, l.ext).c_str(), lc.direct_vox, pool_elem);
+        for (const auto& kv : lc.fft) std::fprintf(fp, " %d %.6e %.6e", kv.first, kv.second.first, kv.second.second);
+        std::fprintf(fp, "\n");
+        f = l.fo;
+      }
+      std::fclose(fp);
+    }
   }
 }
 
