@@ -441,7 +441,9 @@ def main():
                    "parallelism": f"independent halo patches x{ws}",
                    "kernel_spectra": "cached across steps" if cache else "recomputed every step",
                    "planner": ("modelled" if args.no_tune else
-                               f"measured (vxg_model_tune, {t_tune:.1f} s before the timed region)"),
+                               (f"measured costs replayed from {os.environ['VXG_TUNE_FILE']}"
+                                if os.environ.get("VXG_TUNE_FILE") else
+                                f"measured (vxg_model_tune, {t_tune:.1f} s before the timed region)")),
                    "planned_step_s": round(sum(l["seconds"] for l in plan), 4),
                    "layers": " ".join(
                        (f"L{l['layer']}:{l['algo']}" + (f"/T{l['T']}" + ("/tc" if l['tc'] else "/ffma")
