@@ -295,11 +295,12 @@ inline void check_launch(const char* what) {
 // pools (k_pool.cu)
 // MPF of S whole entries (all P fragments); the output may be the channel
 // slice [c0, c0+f) of a tensor with f_tot channels (f_tot <= 0: f)
+// ipz / opz: z row pitch of input / output (0: unpadded)
 void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot = 0,
-                i64 c0 = 0);
+                i64 c0 = 0, i64 ipz = 0, i64 opz = 0);
 void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out);
 void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
-                      const i64* windows, int nwin, float* dense, i64 S0);
+                      const i64* windows, int nwin, float* dense, i64 S0, i64 fpz = 0);
 void launch_nan_check(Ctx* c, const float* x, i64 count);
 bool read_and_clear_flag(Ctx* c);
 
@@ -308,6 +309,6 @@ double bench_ffma(Ctx* c);
 
 // direct convolution (k_direct.cu)
 void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float* w, i64 fo,
-                        V3 k, const float* bias, bool relu, float* out);
+                        V3 k, const float* bias, bool relu, float* out, i64 ipz = 0, i64 opz = 0);
 
 }  // namespace vxg

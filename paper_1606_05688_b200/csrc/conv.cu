@@ -127,6 +127,7 @@ void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, 
   a.src = w;
   a.img_stride = k.vol();
   a.nx = int(k.x); a.ny = int(k.y); a.nz = int(k.z);
+  a.pz = int(k.z);
   a.vx = a.vy = a.vz = 1;
   a.ntx = a.nty = a.ntz = 1;
   a.tiles_per_img = 1;
@@ -143,8 +144,11 @@ void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, 
 
 void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
                      int64_t fo, V3 k, const float* bias, bool relu, float* out,
-                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget) {
+                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget, int64_t ipz,
+                     int64_t opz) {
   const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
+  if (ipz <= 0) ipz = n.z;
+  if (opz <= 0) opz = no.z;
   const int T = plan.T;
   DevBuf wbuf;
   if (!wspec) {
@@ -172,8 +176,9 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     const int64_t mc = std::min(rows, M - m0);
     FwdTileArgs fa{};
     fa.src = in;
-    fa.img_stride = n.vol();
+    fa.img_stride = n.x * n.y * ipz;
     fa.nx = int(n.x); fa.ny = int(n.y); fa.nz = int(n.z);
+    fa.pz = int(ipz);
     fa.vx = int(plan.v.x); fa.vy = int(plan.v.y); fa.vz = int(plan.v.z);
     fa.ntx = int(plan.nt.x); fa.nty = int(plan.nt.y); fa.ntz = int(plan.nt.z);
     fa.tiles_per_img = plan.tiles;
@@ -207,7 +212,8 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ia.fo = fo;
     ia.dst = out;
     ia.onx = int(no.x); ia.ony = int(no.y); ia.onz = int(no.z);
-    ia.oel = no.vol();
+    ia.opz = int(opz);
+    ia.oel = no.x * no.y * opz;
     ia.vx = int(plan.v.x); ia.vy = int(plan.v.y); ia.vz = int(plan.v.z);
     ia.cx = int(k.x - 1); ia.cy = int(k.y - 1); ia.cz = int(k.z - 1);
     ia.ntx = int(plan.nt.x); ia.nty = int(plan.nt.y); ia.ntz = int(plan.nt.z);
@@ -223,12 +229,15 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
 }
 
 void conv_direct_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
-                        int64_t fo, V3 k, const float* bias, bool relu, float* out) {
+                        int64_t fo, V3 k, const float* bias, bool relu, float* out, int64_t ipz,
+                        int64_t opz) {
+  const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
+  if (ipz <= 0) ipz = n.z;
+  if (opz <= 0) opz = no.z;
   for (int64_t s0 = 0; s0 < S; s0 += 65535) {
     const int64_t sn = std::min<int64_t>(65535, S - s0);
-    const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
-    launch_conv_direct(c, in + s0 * f * n.vol(), sn, f, n, w, fo, k, bias, relu,
-                       out + s0 * fo * no.vol());
+    launch_conv_direct(c, in + s0 * f * n.x * n.y * ipz, sn, f, n, w, fo, k, bias, relu,
+                       out + s0 * fo * no.x * no.y * opz, ipz, opz);
   }
 }
 

@@ -12,6 +12,7 @@ struct FwdTileArgs {
   const float* src;
   int64_t img_stride;        // elements per (s, j) image
   int nx, ny, nz;            // image extents
+  int pz = 0;                // z row pitch (elements, >= nz)
   int vx, vy, vz;            // tile step (= valid outputs per tile)
   int ntx, nty, ntz;         // tiles per axis
   int64_t tiles_per_img;
@@ -31,6 +32,7 @@ struct InvTileArgs {
   int64_t fo;
   float* dst;                // (S, fo, on)
   int onx, ony, onz;
+  int opz = 0;               // output z row pitch (>= onz)
   int64_t oel;
   int vx, vy, vz;            // valid outputs per tile
   int cx, cy, cz;            // crop begin inside the tile (k - 1)
@@ -106,11 +108,14 @@ int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo);
 // Conv layer drivers on device pointers.  `wspec` (optional) are cached kernel
 // spectra for plan.T; otherwise computed into scratch.  spectra_budget bounds
 // the per-chunk spectrum buffers (bytes; <= 0: what the context budget leaves).
+// ipz / opz: z row pitch of the input / output activations (0: unpadded)
 void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
                      int64_t fo, V3 k, const float* bias, bool relu, float* out,
-                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget);
+                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget,
+                     int64_t ipz = 0, int64_t opz = 0);
 void conv_direct_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
-                        int64_t fo, V3 k, const float* bias, bool relu, float* out);
+                        int64_t fo, V3 k, const float* bias, bool relu, float* out,
+                        int64_t ipz = 0, int64_t opz = 0);
 
 // rows of spectrum chunk the executor reserves per FFT layer (the chunk grows
 // into whatever the budget leaves; VXG_FFT_ROWS overrides)

@@ -13,6 +13,7 @@
 // fragment tensor in exactly the order recombine_fragments expects.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -25,7 +26,11 @@ namespace vxg {
 
 namespace {
 
-int64_t entry_bytes(const Shape& s) { return s.f * s.n.vol() * 4; }
+// bytes of one batch entry at layer boundary li (z rows padded to the plan's pitch)
+int64_t entry_bytes(const ForwardPlan& p, size_t li) {
+  const Shape& s = p.shapes[li];
+  return s.f * s.n.x * s.n.y * p.pz[li] * 4;
+}
 
 }  // namespace
 
@@ -118,6 +123,18 @@ ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos) const {
     ch.algo = algo;
     p.choice[li] = ch;
   }
+  // Activations between layers get z rows padded to 16 bytes (every bundled
+  // net's extents are odd all the way down), so row starts are aligned for
+  // vector / bulk copies.  The input stays the caller's layout; plain max
+  // pools (unpadded kernel) keep the whole forward unpadded.
+  bool pitched = true;
+  for (size_t li = 0; li < L; ++li)
+    if (net.layers[li].kind == 1 && p.pool_mode[li] != 1) pitched = false;
+  if (const char* e = std::getenv("VXG_NO_PITCH"))
+    if (std::strcmp(e, "0") != 0) pitched = false;
+  p.pz.resize(p.shapes.size());
+  for (size_t i = 0; i < p.shapes.size(); ++i)
+    p.pz[i] = (i == 0 || !pitched) ? p.shapes[i].n.z : (p.shapes[i].n.z + 3) / 4 * 4;
   const Shape& fin = p.shapes.back();
   p.f_out = fin.f;
   p.alpha = fin.s;
@@ -181,16 +198,16 @@ struct Sched {
     return Step{li, li + 1, false, P};
   }
 
-  int64_t in_bytes(size_t li, int64_t B) const { return li >= L ? 0 : B * entry_bytes(p.shapes[li]); }
+  int64_t in_bytes(size_t li, int64_t B) const { return li >= L ? 0 : B * entry_bytes(p, li); }
 
   int64_t out_bytes(const Step& st, int64_t g) const {
     if (st.next >= L) return 0;  // leaves write the final buffer
-    return g * st.P * entry_bytes(p.shapes[st.next]);
+    return g * st.P * entry_bytes(p, st.next);
   }
 
   int64_t ws_bytes(const Step& st, int64_t g) const {
     const Layer& l = m.net.layers[st.li];
-    if (st.fused) return g * std::min<int64_t>(16, l.fo) * p.shapes[st.li + 1].n.vol() * 4;
+    if (st.fused) return g * std::min<int64_t>(16, l.fo) * entry_bytes(p, st.li + 1) / p.shapes[st.li + 1].f;
     if (l.kind != 0 || p.choice[st.li].algo != VXG_CONV_FFT) return 0;
     const LayerChoice& ch = p.choice[st.li];
     const int64_t M = g * ch.fft.tiles;
@@ -284,14 +301,14 @@ struct Runner {
     if (trace_on())
       std::fprintf(stderr, "[vxg] layer %zu: %lld entries, target rows %lld, groups of %lld\n", li,
                    (long long)B, (long long)kTargets[t], (long long)G);
-    const int64_t in_entry = entry_bytes(p.shapes[li]) / 4;
+    const int64_t in_entry = entry_bytes(p, li) / 4;
     for (int64_t b0 = 0; b0 < B; b0 += G) {
       const int64_t g = std::min(G, B - b0);
       const bool leaf = st.next >= L;
       DevBuf out;
       float* dst;
       if (leaf) {
-        dst = final_frags + final_off * (entry_bytes(p.shapes.back()) / 4);
+        dst = final_frags + final_off * (entry_bytes(p, p.shapes.size() - 1) / 4);
       } else {
         out.alloc(m.c, sched.out_bytes(st, g));
         dst = out.as<float>();
@@ -315,7 +332,7 @@ struct Runner {
       const Layer& pool = m.net.layers[li + 1];
       const Shape& mid = p.shapes[li + 1];
       const int ci = m.conv_index[li];
-      const int64_t per_ch = g * mid.n.vol() * 4;
+      const int64_t per_ch = g * mid.n.x * mid.n.y * p.pz[li + 1] * 4;
       int64_t cb = std::max<int64_t>(1, avail() / std::max<int64_t>(per_ch, 1));
       cb = std::min(cb, l.fo);
       if (cb >= 16) cb -= cb % 16;
@@ -325,10 +342,11 @@ struct Runner {
         const int64_t n = std::min(cb, l.fo - c0);
         int h = timer.begin(li);
         conv_direct_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>() + c0 * si.f * kvol,
-                           n, l.ext, m.bias[size_t(ci)].as<float>() + c0, l.relu, tmp.as<float>());
+                           n, l.ext, m.bias[size_t(ci)].as<float>() + c0, l.relu, tmp.as<float>(), p.pz[li],
+                           p.pz[li + 1]);
         timer.end(h);
         h = timer.begin(li + 1);
-        launch_mpf(m.c, tmp.as<float>(), g, n, mid.n, pool.ext, dst, l.fo, c0);
+        launch_mpf(m.c, tmp.as<float>(), g, n, mid.n, pool.ext, dst, l.fo, c0, p.pz[li + 1], p.pz[li + 2]);
         timer.end(h);
       }
       return;
@@ -339,13 +357,14 @@ struct Runner {
       if (p.choice[li].algo == VXG_CONV_FFT) {
         const float2* ws = m.spectra_for(ci, p.choice[li].fft, cache);
         conv_fft_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
-                        m.bias[size_t(ci)].as<float>(), l.relu, dst, p.choice[li].fft, ws, 0);
+                        m.bias[size_t(ci)].as<float>(), l.relu, dst, p.choice[li].fft, ws, 0, p.pz[li],
+                        p.pz[li + 1]);
       } else {
         conv_direct_device(m.c, in, g, si.f, si.n, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
-                           m.bias[size_t(ci)].as<float>(), l.relu, dst);
+                           m.bias[size_t(ci)].as<float>(), l.relu, dst, p.pz[li], p.pz[li + 1]);
       }
     } else if (p.pool_mode[li] == 1) {
-      launch_mpf(m.c, in, g, si.f, si.n, l.ext, dst);
+      launch_mpf(m.c, in, g, si.f, si.n, l.ext, dst, 0, 0, p.pz[li], p.pz[li + 1]);
     } else {
       launch_maxpool(m.c, in, g, si.f, si.n, l.ext, dst);
     }
@@ -387,8 +406,8 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows)
       t = i;
       break;
     }
-  const int64_t in = p.S * entry_bytes(p.shapes[0]);
-  const int64_t frags = p.S * p.alpha * entry_bytes(p.shapes.back());
+  const int64_t in = p.S * entry_bytes(p, 0);
+  const int64_t frags = p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1);
   const int64_t dense = p.S * p.f_out * p.dense.vol() * 4;
   int64_t spectra_bytes = 0;
   (void)cache;  // spectra are resident for the whole forward either way
@@ -407,7 +426,7 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows)
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
                     std::vector<double>* layer_seconds) {
   EventTimer timer(c->stream, layer_seconds != nullptr);
-  DevBuf frags(c, p.S * p.alpha * entry_bytes(p.shapes.back()));
+  DevBuf frags(c, p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1));
   // kernel spectra first, so the group sizes below see their footprint
   for (size_t li = 0; li < net.layers.size(); ++li)
     if (net.layers[li].kind == 0 && p.choice[li].algo == VXG_CONV_FFT) {
@@ -447,12 +466,14 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
   if (!cache) spectra.clear();  // stream-ordered frees: recomputed by the next forward
   const size_t nwin = p.windows.size() / 3;
   if (nwin == 0) {
-    VXG_CUDA_CHECK(cudaMemcpyAsync(d_dense, frags.get(), size_t(frags.bytes()),
-                                   cudaMemcpyDeviceToDevice, c->stream));
+    const Shape& fin = p.shapes.back();
+    VXG_CUDA_CHECK(cudaMemcpy2DAsync(d_dense, size_t(fin.n.z) * 4, frags.get(), size_t(p.pz.back()) * 4,
+                                     size_t(fin.n.z) * 4, size_t(p.S * fin.f * fin.n.x * fin.n.y),
+                                     cudaMemcpyDeviceToDevice, c->stream));
   } else {
     const Shape& fin = p.shapes.back();
     launch_recombine(c, frags.as<float>(), p.S * p.alpha, 0, fin.f, fin.n, p.windows.data(),
-                     int(nwin), d_dense, p.S);
+                     int(nwin), d_dense, p.S, p.pz.back());
   }
   timer.collect(layer_seconds, net.layers.size());
 }

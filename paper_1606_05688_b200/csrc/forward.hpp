@@ -26,6 +26,7 @@ struct ForwardPlan {
   std::vector<LayerChoice> choice;    // per layer (conv layers only meaningful)
   std::vector<int> pool_mode;         // per layer: 1 fragments, 0 plain (pools only)
   std::vector<int64_t> windows;       // fragment windows (network order), flat x3
+  std::vector<int64_t> pz;            // z row pitch per layer boundary (0: the input, unpadded)
   int64_t S = 1;
   V3 dense;
   int64_t f_out = 1;

@@ -23,6 +23,7 @@ struct DirectGeom {
   int nx, ny, nz;
   int kx, ky, kz;
   int ox, oy, oz;           // output extents
+  int ipz, opz;             // z row pitch of input / output
   int tiles_x, tiles_y, tiles_z;
   int relu;
 };
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(THREADS) conv_direct_kernel(const float* __res
 #pragma unroll
     for (int r = 0; r < ZR; ++r) acc[j][r] = 0.f;
 
-  const int64_t nel = int64_t(g.nx) * g.ny * g.nz;
+  const int64_t nel = int64_t(g.nx) * g.ny * g.ipz;
   for (int64_t i = 0; i < g.f; ++i) {
     __syncthreads();
     // weights of maps j0..j0+15 for input map i, transposed to [q][j]
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(THREADS) conv_direct_kernel(const float* __res
       const int zz = t % bz, yy = (t / bz) % by, xx = t / (bz * by);
       const int gx = tx0 + xx, gy = ty0 + yy, gz = tz0 + zz;
       float v = 0.f;
-      if (gx < g.nx && gy < g.ny && gz < g.nz) v = __ldg(src + (int64_t(gx) * g.ny + gy) * g.nz + gz);
+      if (gx < g.nx && gy < g.ny && gz < g.nz) v = __ldg(src + (int64_t(gx) * g.ny + gy) * g.ipz + gz);
       is[t] = v;
     }
     __syncthreads();
@@ -124,12 +125,12 @@ __global__ void __launch_bounds__(THREADS) conv_direct_kernel(const float* __res
 
   const int gx = tx0 + lx, gy = ty0 + ly;
   if (gx >= g.ox || gy >= g.oy) return;
-  const int64_t oel = int64_t(g.ox) * g.oy * g.oz;
+  const int64_t oel = int64_t(g.ox) * g.oy * g.opz;
 #pragma unroll
   for (int j = 0; j < JB; ++j) {
     if (j0 + j >= g.fo) break;
     const float b = __ldg(bias + j0 + j);
-    float* o = out + (s * g.fo + j0 + j) * oel + (int64_t(gx) * g.oy + gy) * g.oz;
+    float* o = out + (s * g.fo + j0 + j) * oel + (int64_t(gx) * g.oy + gy) * g.opz;
 #pragma unroll
     for (int r = 0; r < ZR; ++r) {
       const int gz = tz0 + lz + r;
@@ -169,12 +170,14 @@ void run_direct(Ctx* c, const float* in, const float* w, const float* bias, floa
 }  // namespace
 
 void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float* w, i64 fo,
-                        V3 k, const float* bias, bool relu, float* out) {
+                        V3 k, const float* bias, bool relu, float* out, i64 ipz, i64 opz) {
   DirectGeom g{};
   g.S = S; g.f = f; g.fo = fo;
   g.nx = int(n.x); g.ny = int(n.y); g.nz = int(n.z);
   g.kx = int(k.x); g.ky = int(k.y); g.kz = int(k.z);
   g.ox = int(n.x - k.x + 1); g.oy = int(n.y - k.y + 1); g.oz = int(n.z - k.z + 1);
+  g.ipz = int(ipz > 0 ? ipz : n.z);
+  g.opz = int(opz > 0 ? opz : g.oz);
   g.tiles_x = (g.ox + TX - 1) / TX;
   g.tiles_y = (g.oy + TY - 1) / TY;
   g.tiles_z = (g.oz + TZ - 1) / TZ;

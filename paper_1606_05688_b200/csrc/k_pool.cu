@@ -111,6 +111,7 @@ struct MpfGeom {
   int f_tot, c0;        // output channel count and offset
   int tiles_z, tiles_y, tiles_x;
   int64_t planes;       // S * f
+  int ipz, opz;         // z row pitch of input / output planes
 };
 
 constexpr int MPF_TZ = 32, MPF_TY = 8, MPF_XT = 16;
@@ -128,8 +129,8 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
   const int x1 = min(x0 + MPF_XT, g.dx);
   const bool live = z < g.dz && y < g.dy;
   bool saw_nan = false;
-  const int64_t nel = int64_t(g.nx) * g.ny * g.nz;
-  const int moel = g.mx * g.my * g.mz;
+  const int64_t nel = int64_t(g.nx) * g.ny * g.ipz;
+  const int moel = g.mx * g.my * g.opz;
   const int zo = z / pz, yo = y / py;
   const int offyz = (y % py) * pz + (z % pz);
   for (int64_t plane = blockIdx.y; plane < g.planes; plane += gridDim.y) {
@@ -137,18 +138,18 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
     const int64_t s = plane / g.f;
     const int fm = int(plane % g.f);
     const float* src = in + plane * nel;
-    float* dst0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(yo) * g.mz + zo;
+    float* dst0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(yo) * g.opz + zo;
     const int64_t fstride = int64_t(g.f_tot) * moel;  // one fragment further
     if (PX == 2 && PY == 2 && PZ == 2 && x1 - x0 == MPF_XT && z + 1 < g.nz && y + 1 < g.ny) {
       // hot path: all 4 * (XT + 1) loads issued before any use
       float v[MPF_XT + 1][4];
 #pragma unroll
       for (int r = 0; r <= MPF_XT; ++r) {
-        const float* row = src + (int64_t(x0 + r) * g.ny + y) * g.nz + z;
+        const float* row = src + (int64_t(x0 + r) * g.ny + y) * g.ipz + z;
         v[r][0] = __ldg(row);
         v[r][1] = __ldg(row + 1);
-        v[r][2] = __ldg(row + g.nz);
-        v[r][3] = __ldg(row + g.nz + 1);
+        v[r][2] = __ldg(row + g.ipz);
+        v[r][3] = __ldg(row + g.ipz + 1);
       }
       float prev = 0.f;
 #pragma unroll
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
           const int xd = x0 + r - 1;
           const float d = m > prev ? m : prev;
           const int off = (xd & 1) * 4 + offyz;
-          dst0[off * fstride + int64_t(xd >> 1) * g.my * g.mz] = d;
+          dst0[off * fstride + int64_t(xd >> 1) * g.my * g.opz] = d;
         }
         prev = m;
       }
@@ -172,13 +173,13 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
     }
     float r[8];                                       // ring of row maxima (px <= 8)
     for (int x = x0; x < x1 + px - 1; ++x) {
-      const float* row = src + (int64_t(x) * g.ny + y) * g.nz + z;
+      const float* row = src + (int64_t(x) * g.ny + y) * g.ipz + z;
       float m = __ldg(row);
 #pragma unroll
       for (int qy = 0; qy < py; ++qy)
 #pragma unroll
         for (int qz = 0; qz < pz; ++qz) {
-          const float v = __ldg(row + qy * g.nz + qz);
+          const float v = __ldg(row + qy * g.ipz + qz);
           saw_nan |= (v != v);
           m = v > m ? v : m;
         }
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
         float d = r[0];
         for (int i = 1; i < px; ++i) d = r[i] > d ? r[i] : d;
         const int off = (xd % px) * py * pz + offyz;
-        dst0[off * fstride + int64_t(xd / px) * g.my * g.mz] = d;
+        dst0[off * fstride + int64_t(xd / px) * g.my * g.opz] = d;
       }
     }
   }
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
   const int z = z0 + 2 * lz, y = y0 + ly;  // columns z (even) and z + 1
   const int x1 = min(M2_XT, g.dx - x0);
   const bool live = z < g.dz && y < g.dy;    // dz is even: z + 1 < dz too
-  const int64_t nel = int64_t(g.nx) * g.ny * g.nz;
-  const int moel = g.mx * g.my * g.mz;
+  const int64_t nel = int64_t(g.nx) * g.ny * g.ipz;
+  const int moel = g.mx * g.my * g.opz;
   const int64_t fstride = int64_t(g.f_tot) * moel;
   const int offy = (y & 1) * 2;
   bool saw_nan = false;
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
         const int bx = r / M2_BY, by = r % M2_BY;
         const int gx = x0 + bx, gy = y0 + by;
         const bool rok = gx < g.nx && gy < g.ny;
-        const float* row = src + (int64_t(gx) * g.ny + gy) * g.nz + z0;
+        const float* row = src + (int64_t(gx) * g.ny + gy) * g.ipz + z0;
 #pragma unroll
         for (int bz = lane; bz < M2_BZ; bz += 32) {
           const bool ok = rok && z0 + bz < g.nz;
@@ -259,9 +260,9 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     if (!live) continue;
     const int64_t s = plane / g.f;
     const int fm = int(plane % g.f);
-    const int64_t mstep = int64_t(g.my) * g.mz;  // one fragment x row
+    const int64_t mstep = int64_t(g.my) * g.opz;  // one fragment x row
     // fragment pointers for D row parity (x even / odd) and column parity
-    float* q0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.mz +
+    float* q0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.opz +
                 (z >> 1) + int64_t(x0 >> 1) * mstep;
     float* qe0 = q0 + int64_t(0 + offy) * fstride;
     float* qe1 = q0 + int64_t(1 + offy) * fstride;
@@ -322,6 +323,7 @@ __global__ void nan_check_kernel(const float* __restrict__ x, int64_t n, int* fl
 // with the FIRST window slowest (layers.hpp:494-504).
 struct RecGeom {
   int64_t nx, ny, nz;        // fragment extents
+  int64_t fpz;               // fragment z row pitch
   int64_t dx, dy, dz;        // dense extents
   int64_t sx, sy, sz;        // total stride per axis
   int64_t f, alpha, S0;
@@ -356,9 +358,9 @@ __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict_
   const int64_t fm = sf % g.f, s = sf / g.f;
   for (int o = threadIdx.x; o < g.sz; o += blockDim.x) ztab[o] = frag_term(g, o, 2);
   __syncthreads();
-  const int64_t nel = g.nx * g.ny * g.nz;
+  const int64_t nel = g.nx * g.ny * g.fpz;
   const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
-  const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.nz;
+  const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz;
   float* dst = dense + row * g.dz;
   const int sz = int(g.sz);
   const int64_t fstride = g.f * nel;
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict_
 }  // namespace
 
 void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot,
-                i64 c0) {
+                i64 c0, i64 ipz, i64 opz) {
   require(p.x <= 8, "mpf: window above 8 along x");
   MpfGeom g{};
   g.nx = int(n.x); g.ny = int(n.y); g.nz = int(n.z);
@@ -385,6 +387,8 @@ void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i
   g.tiles_y = (g.dy + MPF_TY - 1) / MPF_TY;
   g.tiles_x = (g.dx + MPF_XT - 1) / MPF_XT;
   g.planes = S * f;
+  g.ipz = int(ipz > 0 ? ipz : n.z);
+  g.opz = int(opz > 0 ? opz : g.mz);
   const int64_t tiles = int64_t(g.tiles_z) * g.tiles_y * g.tiles_x;
   if (tiles == 0 || g.planes == 0) return;
   require(tiles < (int64_t(1) << 31), "mpf: grid too large");
@@ -412,11 +416,12 @@ void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* ou
 }
 
 void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
-                      const i64* windows, int nwin, float* dense, i64 S0) {
+                      const i64* windows, int nwin, float* dense, i64 S0, i64 fpz) {
   require(nwin <= 8, "recombine: at most 8 fragment windows supported");
   require(b0 == 0, "recombine: partial fragment ranges are not supported");
   RecGeom g{};
   g.nx = n.x; g.ny = n.y; g.nz = n.z;
+  g.fpz = fpz > 0 ? fpz : n.z;
   g.f = f; g.S0 = S0; g.nwin = nwin;
   int64_t stride[3] = {1, 1, 1};
   int64_t alpha = 1;

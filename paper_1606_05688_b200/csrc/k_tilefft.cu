@@ -118,12 +118,12 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
       // interior box (the common case): no bounds tests, one LDGSTS per row
       if (lane < T) {
         for (int x = warp; x < T; x += NWARPS) {
-          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.nz + gz;
+          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.pz + gz;
           float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 8
           for (int y = 0; y < T; ++y) {
             cp_async4(d + 2 * C::SY * y, g, true);
-            g += a.nz;
+            g += a.pz;
           }
         }
       }
@@ -132,13 +132,13 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
       for (int x = warp; x < T; x += NWARPS) {
         const int gx = ox + x;
         const bool xin = zin && gx < a.nx;
-        const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
+        const float* g = img + (int64_t(gx) * a.ny + oy) * a.pz + gz;
         float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 4
         for (int y = 0; y < T; ++y) {
           const bool in = xin && oy + y < a.ny;
           if (lane < T) cp_async4(d, in ? g : img, in);
-          g += a.nz;
+          g += a.pz;
           d += 2 * C::SY;
         }
       }
@@ -303,12 +303,12 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdT
     if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
       if (lane < T) {
         for (int x = warp; x < HP; x += NWARPS) {
-          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.nz + gz;
+          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.pz + gz;
           float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 8
           for (int y = 0; y < T; ++y) {
             cp_async4(d + 2 * C::SY * y, g, true);
-            g += a.nz;
+            g += a.pz;
           }
         }
       }
@@ -317,13 +317,13 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdT
       for (int x = warp; x < HP; x += NWARPS) {
         const int gx = ox + x;
         const bool xin = zin && gx < a.nx;
-        const float* g = img + (int64_t(gx) * a.ny + oy) * a.nz + gz;
+        const float* g = img + (int64_t(gx) * a.ny + oy) * a.pz + gz;
         float* d = spf + 2 * (x * C::SX) + lane;
 #pragma unroll 4
         for (int y = 0; y < T; ++y) {
           const bool in = xin && oy + y < a.ny;
           if (lane < T) cp_async4(d, in ? g : img, in);
-          g += a.nz;
+          g += a.pz;
           d += 2 * C::SY;
         }
       }
@@ -547,12 +547,12 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
     for (int x = warp; x < a.vx; x += NWARPS) {
       const int gx = gx0 + x;
       if (!zin || gx >= a.onx) continue;
-      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.onz + gz;
+      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.opz + gz;
       const float* r = spf + 2 * ((a.cx + x) * C::SX + a.cy * C::SY) + a.cz + lane;
 #pragma unroll 4
       for (int y = 0; y < ylim; ++y) {
         *o = *r;
-        o += a.onz;
+        o += a.opz;
         r += 2 * C::SY;
       }
     }
@@ -726,12 +726,12 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
     for (int xx = warp; xx < nxl; xx += NWARPS) {
       const int gx = tx * a.vx + (xa - a.cx) + xx;
       if (!zin || gx >= a.onx) continue;
-      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.onz + gz;
+      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.opz + gz;
       const float* rr = spf + 2 * ((xa - x0 + xx) * C::SX + a.cy * C::SY) + a.cz + lane;
 #pragma unroll 4
       for (int y = 0; y < ylim; ++y) {
         *o = *rr;
-        o += a.onz;
+        o += a.opz;
         rr += 2 * C::SY;
       }
     }
