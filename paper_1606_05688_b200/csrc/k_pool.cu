@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(256) mpf_full_kernel(const float* __restrict__
 // Each thread owns two adjacent z columns so a warp writes 32 consecutive
 // floats (a full 128-byte line) into each of the two z-parity fragments.
 constexpr int M2_TZ = 64, M2_TY = 8, M2_XT = 16;
-constexpr int M2_BZ = M2_TZ + 2, M2_BY = M2_TY + 1, M2_BX = M2_XT + 1;  // row padded to even
+// box rows padded to 68 floats (16-byte multiple): with 16-byte aligned input
+// rows (the network forward's padded pitch) a row is 17 16-byte copies
+constexpr int M2_BZ = M2_TZ + 4, M2_BY = M2_TY + 1, M2_BX = M2_XT + 1;
 
 __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ in,
                                                      float* __restrict__ out, MpfGeom g,
@@ -229,11 +231,23 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
   const int moel = g.mx * g.my * g.opz;
   const int64_t fstride = int64_t(g.f_tot) * moel;
   const int offy = (y & 1) * 2;
+  const bool vec = (g.ipz & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
   bool saw_nan = false;
   for (int64_t plane = blockIdx.y; plane < g.planes; plane += gridDim.y) {
     const float* src = in + plane * nel;
     __syncthreads();  // previous plane's readers are done with the box
-    {
+    if (vec) {
+      // 16-byte copies: thread per (row, chunk); chunks past the row pitch are
+      // zero-filled (the padding inside it is never used nor NaN-scanned)
+      for (int u = threadIdx.x; u < M2_BX * M2_BY * (M2_BZ / 4); u += 256) {
+        const int r = u / (M2_BZ / 4), ch = u % (M2_BZ / 4);
+        const int bx = r / M2_BY, by = r % M2_BY;
+        const int gx = x0 + bx, gy = y0 + by;
+        const bool ok = gx < g.nx && gy < g.ny && z0 + 4 * ch < g.ipz;
+        const float* row = src + (int64_t(gx) * g.ny + gy) * g.ipz + z0 + 4 * ch;
+        cp_async16(&box[r * M2_BZ + 4 * ch], ok ? row : src, ok);
+      }
+    } else {
       // warp per box row, lane = z (coalesced 4-byte copies)
       const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
       for (int r = w; r < M2_BX * M2_BY; r += 8) {
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     // staged element once, instead of per use in the window loop
     for (int e = threadIdx.x; e < M2_BX * M2_BY * M2_BZ; e += 256) {
       const float v = box[e];
-      saw_nan |= v != v;
+      saw_nan |= (v != v) && (z0 + e % M2_BZ < g.nz);
     }
     if (!live) continue;
     const int64_t s = plane / g.f;
