@@ -304,6 +304,12 @@ def main():
     if not args.no_tune:
         model.tune(1, e)
         e, algos = choose(True)
+    if ws > 1:
+        # every rank processes rank 0's patch shape (its own tile of the volume),
+        # so value = ws * voxels is exact even if per-rank timings differ
+        pick = [e, algos]
+        dist.broadcast_object_list(pick, src=0)
+        e, algos = pick
     t_tune = time.perf_counter() - t_tune
     plan = model.plan_info(1, e, algos)
     dense = e - fov + 1
