@@ -267,9 +267,23 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     __syncthreads();
     // NaN scan of the staged box (mpf_pool rejects NaN, layers.hpp:429): each
     // staged element once, instead of per use in the window loop
-    for (int e = threadIdx.x; e < M2_BX * M2_BY * M2_BZ; e += 256) {
-      const float v = box[e];
-      saw_nan |= (v != v) && (z0 + e % M2_BZ < g.nz);
+    // 16-byte reads; only a box reaching past nz masks its tail (the row
+    // padding is never written and may hold anything)
+    {
+      const int zlim = g.nz - z0;  // valid z in the box: [0, zlim)
+      const float4* b4 = reinterpret_cast<const float4*>(box);
+      for (int u = threadIdx.x; u < M2_BX * M2_BY * (M2_BZ / 4); u += 256) {
+        const float4 v = b4[u];
+        const int zc = 4 * (u % (M2_BZ / 4));
+        bool n = false;
+        if (zc + 3 < zlim) {
+          n = (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
+        } else {
+          n = ((v.x != v.x) && zc < zlim) | ((v.y != v.y) && zc + 1 < zlim) | ((v.z != v.z) && zc + 2 < zlim) |
+              ((v.w != v.w) && zc + 3 < zlim);
+        }
+        saw_nan |= n;
+      }
     }
     if (!live) continue;
     const int64_t s = plane / g.f;
