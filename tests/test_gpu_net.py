@@ -180,3 +180,37 @@ def test_tiled_volume_equals_whole_volume(ctx):
     assert dense.shape == (1, 3, 56, 48, 40)
     err = np.abs(dense[:, :, :48, :48, :40] - full).max() / np.abs(full).max()
     assert err <= TOL, err
+
+
+def test_bench_patch_full_size_vs_direct_crops(ctx):
+    """BASELINE-size parity (SURVEY 8c recipe): n537 on the bench's 722^3 patch
+    with the bench's plan (measured planner, direct first layer, tensor-core FFT
+    layers), checked at three random 16^3 output blocks against all-direct
+    forwards of the matching 186^3 input crops (an independent algorithm: fp32
+    FFMA direct convolution, no spectra), translation equivariance making the
+    crops exact sub-problems."""
+    import torch
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n537"])
+    e, c = 722, 186
+    fov = int(net.field_of_view()[0])
+    model = v.Model(net, v.random_weights(net, 1), ctx)
+    algos = ["direct"] + ["auto"] * (net.conv_count - 1)
+    model.tune(1, e)
+    plan = model.plan_info(1, e, algos)
+    assert any(l.get("tc") for l in plan if l["kind"] == "conv"), plan
+    x = torch.from_numpy(v.fill_random((1, 1, e, e, e), 11)).cuda()
+    full, _ = model.forward(x, conv_algos=algos)
+    assert tuple(full.shape) == (1, 3, e - fov + 1, e - fov + 1, e - fov + 1)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        o = [int(t) for t in rng.integers(0, e - c + 1, size=3)]
+        crop = x[:, :, o[0]:o[0] + c, o[1]:o[1] + c, o[2]:o[2] + c].contiguous()
+        part, _ = model.forward(crop, conv_algos="direct")
+        n = c - fov + 1
+        ref = full[:, :, o[0]:o[0] + n, o[1]:o[1] + n, o[2]:o[2] + n]
+        err = ((part - ref).abs().max() / part.abs().max()).item()
+        assert err <= TOL, (o, err)
+    del full
+    torch.cuda.empty_cache()
