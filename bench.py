@@ -369,7 +369,9 @@ def main():
     out_host = torch.empty((1, fout, dense, dense, dense), dtype=torch.float32).pin_memory()
     xin = x_pin.numpy()
     oh = out_host.numpy()
-    model.forward(xin, out=oh, conv_algos=algos, cache_spectra=cache)  # warm
+    # warm the streaming path itself: its double buffers change the forward's
+    # arena size, and the pool maps a block of the new size only once
+    model.forward_many([xin] * 2, outputs=[oh] * 2, conv_algos=algos, cache_spectra=cache)
     if ws > 1:
         dist.barrier()
     # the streaming API (the tiler's path): every step uploads its patch and

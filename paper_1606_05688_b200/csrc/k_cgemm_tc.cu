@@ -44,12 +44,12 @@
 #include "async.cuh"
 #include "common.cuh"
 #include "fftconv.hpp"
+#include "tcgen05.cuh"
 
 namespace vxg {
 namespace {
 
-constexpr int TC_M = 128;
-constexpr int TC_KC = 8;
+using namespace tc;
 constexpr int TC_SLOTS = 3;
 constexpr int TC_THREADS = 384;  // 12 warps
 constexpr int RAW_ROW = 144;     // padded raw-row stride (bytes)
@@ -66,95 +66,6 @@ struct TcCfg {
   static constexpr int STAGE = 4 * 4096;  // pair-major epilogue: 4 KB transpose tile per warp
   static constexpr int SMEM = TC_SLOTS * SLOT + STAGE + 128;
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// K-major, no swizzle: core matrix = 8 rows x 16 B contiguous; LBO = 128 B
-// between the two K halves, SBO = 256 B between 8-row groups; version 1.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
-         (uint64_t(1) << 46);
-}
-
-// byte offset of (row, k-group of 4) in a K-major 8-wide tile
-__host__ __device__ __forceinline__ int tile_off(int row, int kgroup) {
-  return (row >> 3) * 256 + kgroup * 128 + (row & 7) * 16;
-}
-
-__device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // exactly representable in tf32
-  lo = v - hi;                                             // exact in fp32
-}
-
-template <int N>
-__device__ __forceinline__ constexpr uint32_t idesc_tf32(bool neg_b) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(neg_b) << 14) | (uint32_t(N >> 3) << 17) |
-         (uint32_t(TC_M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
-}
-
-// A operand from tensor memory (row = lane, K along columns): the MMA then
-// reads only B from shared memory
-__device__ __forceinline__ void mma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;\n" ::"r"(bytes),
-               "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_copy(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
 
 // ---- one-time W preparation: raw [w/16][i][j][16] complex -> per (pair, chunk)
 // the 8 matrices (w, re/im, hi/lo) of FO x 8 tf32 in the UMMA layout.

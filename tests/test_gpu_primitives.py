@@ -171,6 +171,31 @@ def test_conv_random_vs_oracle(oracle, ctx, case):
     assert rel_error(v.conv_fft_staged(x, p, ctx).output, want) <= 1e-4
 
 
+@pytest.mark.parametrize("case", [
+    (2, (30, 20, 300), 80, (2, 2, 2)),
+    (1, (17, 19, 140), 48, (3, 3, 3)),
+    (2, (24, 21, 131), 64, (4, 4, 4)),
+    (1, (9, 10, 257), 80, (4, 3, 2)),
+    (1, (9, 10, 40), 32, (4, 4, 4)),   # 32 maps: FFMA kernel
+])
+def test_conv_direct_single_input_map_tensor_cores(oracle, ctx, case):
+    """f = 1 direct convolution (the first layer of every bundled net) on the
+    tcgen05 implicit-GEMM kernel (48..80 maps per launch): several 128-voxel z
+    tiles with a ragged last one, k^3 taps padded to 8/32/64, anisotropic
+    kernels; against the C oracle (fp64)."""
+    import paper_1606_05688_b200 as v
+    S, n, fo, k = case
+    rng = np.random.default_rng(sum(n) + fo)
+    x = rng.uniform(-1, 1, (S, 1) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, 1) + k) * np.sqrt(3.0 / np.prod(k))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    want = oracle.conv(x, w, b, True)
+    got = v.conv_direct(x, v.ConvLayerParams(w, b, "relu"), ctx).output
+    assert rel_error(got, want) <= 1e-5
+    lin = v.conv_direct(x, v.ConvLayerParams(w, b, "identity"), ctx).output
+    assert rel_error(lin, oracle.conv(x, w, b, False)) <= 1e-5
+
+
 @pytest.mark.parametrize("variant", ["tc_pair", "tc_single", "ffma"])
 def test_conv_fft_every_tile_size_vs_oracle(oracle, ctx, variant):
     """Every tile FFT size the planner may pick, each contraction and forward
