@@ -626,8 +626,16 @@ void Model::tune(int64_t S, V3 e) {
         const V3 ns{d + k.x - 1, d + k.y - 1, d + k.z - 1};
         DevBuf x(c, f * ns.vol() * 4), y(c, fo * d * d * d * 4);
         fill_sample(c, x.as<float>(), f * ns.vol(), 777u);
+        // followed by an MPF, the forward fuses the two by channel blocks whose
+        // width the free memory sets (16 at the big patches the planner is for);
+        // time that block width, since the kernel choice depends on it
+        const bool fused = li + 1 < p0.shapes.size() - 1 && net.layers[li + 1].kind == 1 &&
+                           p0.pool_mode[li + 1] == 1;
+        const int64_t cb = fused ? std::min<int64_t>(16, fo) : fo;
         const double t = time_on_stream(c, [&] {
-          conv_direct_device(c, x.as<float>(), 1, f, ns, w, fo, k, b, l.relu, y.as<float>());
+          for (int64_t c0 = 0; c0 < fo; c0 += cb)
+            conv_direct_device(c, x.as<float>(), 1, f, ns, w + c0 * f * k.vol(), std::min(cb, fo - c0), k,
+                               b + c0, l.relu, y.as<float>() + c0 * d * d * d);
         }, 2);
         lc.direct_vox = t / double(d * d * d);
       }
