@@ -33,8 +33,8 @@ NET = "n537"
 # reference runs there
 SMALLEST = {"n337": 92, "n537": 170, "n726": 120, "n926": 158}
 # ncu DRAM bytes per launch / the launch's algorithmic bytes (profiles/r1_ncu_summary.md):
-# cgemm_tc (M = 1728 rows, T = 32): (24.45 + 19.73) GB / (2 x 19.26 GB X, Y + 1.78 GB W)
-TRAFFIC_RATIO = {"cgemm": round((24.45 + 19.73) / (2 * 19.26 + 1.78), 3)}
+# cgemm_tc (M = 1728 rows, T = 32, final capture r1e): (21.89 + 19.82) GB / (2 x 19.26 GB X, Y + 1.78 GB W)
+TRAFFIC_RATIO = {"cgemm": round((21.89 + 19.82) / (2 * 19.26 + 1.78), 3)}
 FFMA_FALLBACK_TFLOPS = 74.4  # 148 SM x 128 x 2 x 1.965 GHz (nominal), used only if measurement fails
 
 

@@ -8,9 +8,11 @@
 // kind::tf32 with the 3xTF32 split of k_cgemm_tc.cu (fp32-level accuracy).
 //
 // Persistent CTAs (one per SM), warp-specialised like the contraction:
-//   warps 0,2,3 producers: cp.async of the kx*ky input row segments of a tile
-//               (128 + kz - 1 floats each, zero past the image) into a
-//               4-slot ring;
+//   warps 0,2,3 producers: the kx*ky input row segments of a tile (128 + kz - 1
+//               floats each, zero past the image) into a 4-slot ring, by
+//               16-byte cp.async of each segment's aligned superset (the
+//               row's misalignment recorded per slot) when the input is
+//               16-byte aligned, else 4-byte copies;
 //   warps 8-11  converters: row m gathers its k^3 taps from the staged rows,
 //               splits them into tf32 hi/lo and writes them to TMEM (A of
 //               buffer t % 2);
@@ -50,6 +52,7 @@ struct DtGeom {
   int ztiles;
   int64_t tiles;
   int relu;
+  int vec;  // input 16-byte aligned: rows staged by 16-byte copies of aligned supersets
 };
 
 template <int N, int K>
@@ -59,6 +62,8 @@ struct DtCfg {
   static constexpr int SLOT = DT_ROWS * DT_RS * 4;
   static constexpr int OFF_BIAS = 512;   // N floats
   static constexpr int OFF_TAPS = 1024;  // K ints: staged-row offset of tap q (-1: padding)
+  static constexpr int OFF_SHIFT = 1280; // [slot][row] ints: where a staged row's z0 lands (16-byte path)
+  static constexpr int OFF_TROW = 1536;  // K ints: staged row of tap q
   static constexpr int OFF_W = 2048;
   static constexpr int OFF_RING = OFF_W + W_BYTES;
   static constexpr int SMEM = OFF_RING + DT_NS * SLOT;
@@ -105,6 +110,8 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* sbias = reinterpret_cast<float*>(smem + C::OFF_BIAS);
   int* staps = reinterpret_cast<int*>(smem + C::OFF_TAPS);
+  int* sshift = reinterpret_cast<int*>(smem + C::OFF_SHIFT);
+  int* strow = reinterpret_cast<int*>(smem + C::OFF_TROW);
   uint8_t* sw = smem + C::OFF_W;
   float* ring = reinterpret_cast<float*>(smem + C::OFF_RING);
 
@@ -126,12 +133,14 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   // in[p + k-1-q] (true convolution): tap q = (qx, qy, qz) reads staged row
   // (kx-1-qx, ky-1-qy) at column m + kz-1-qz
   for (int q = tid; q < K; q += DT_THREADS) {
-    int off = -1;
+    int off = -1, row = 0;
     if (q < g.kvol) {
       const int qz = q % g.kz, qy = (q / g.kz) % g.ky, qx = q / (g.kz * g.ky);
-      off = ((g.kx - 1 - qx) * g.ky + (g.ky - 1 - qy)) * DT_RS + (g.kz - 1 - qz);
+      row = (g.kx - 1 - qx) * g.ky + (g.ky - 1 - qy);
+      off = row * DT_RS + (g.kz - 1 - qz);
     }
     staps[q] = off;
+    strow[q] = row;
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   }
   if (tid == 32) {
     for (int s = 0; s < DT_NS; ++s) {
-      mbar_init(&full[s], 96);  // 3 producer warps' cp.async arrivals
+      mbar_init(&full[s], 96 + 3);  // 3 producer warps' cp.async arrivals + their shift-table arrives
       mbar_init(&slot_empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
@@ -184,13 +193,33 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       const float* img = g.in + si * int64_t(g.nx) * g.ny * g.ipz;
       for (int r = pw; r < nrows; r += 3) {
         const int a = r / g.ky, b = r % g.ky;
-        const float* row = img + (int64_t(x + a) * g.ny + (y + b)) * g.ipz;
-        for (int zz = lane; zz < rlen; zz += 32) {
-          const bool ok = z0 + zz < g.nz;
-          cp_async4(dst + r * DT_RS + zz, ok ? row + z0 + zz : row, ok);
+        const int64_t rowoff = (si * g.nx + (x + a)) * int64_t(g.ny) * g.ipz + int64_t(y + b) * g.ipz;
+        if (g.vec) {
+          // the aligned superset [o - sh, ...) of the row segment by 16-byte
+          // copies (zero past nz); the converters read it at +sh
+          const int64_t o = rowoff + z0;
+          const int sh = int(o & 3);
+          const int64_t oa = o - sh, rend = rowoff + g.nz;
+          const int nch = (rlen + sh + 3) >> 2;
+          for (int ch = lane; ch < nch; ch += 32) {
+            const int64_t e = oa + 4 * ch;
+            const int64_t valid = rend - e < 0 ? 0 : (rend - e > 4 ? 4 : rend - e);
+            const unsigned sdst = static_cast<unsigned>(__cvta_generic_to_shared(dst + r * DT_RS + 4 * ch));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst),
+                         "l"(valid > 0 ? g.in + e : g.in), "r"(int(valid * 4)));
+          }
+          if (lane == 0) sshift[s * DT_ROWS + r] = sh;
+        } else {
+          const float* row = img + (int64_t(x + a) * g.ny + (y + b)) * g.ipz;
+          for (int zz = lane; zz < rlen; zz += 32) {
+            const bool ok = z0 + zz < g.nz;
+            cp_async4(dst + r * DT_RS + zz, ok ? row + z0 + zz : row, ok);
+          }
+          if (lane == 0) sshift[s * DT_ROWS + r] = 0;
         }
       }
       cp_async_arrive_noinc(&full[s]);
+      if (lane == 0) mbar_arrive(&full[s]);  // releases this warp's shift-table entries
     }
   } else if (warp >= 8) {
     // ---------------- converters: thread m owns output voxel z0 + m ----------------
@@ -202,13 +231,14 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       if (lt >= 2) mbar_wait(&a_empty[b], uint32_t((lt / 2 - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const float* src = ring + s * (DT_ROWS * DT_RS) + m;
+      const int* shs = sshift + s * DT_ROWS;
 #pragma unroll 1
       for (int q0 = 0; q0 < K; q0 += KC) {
         uint32_t hi[KC], lo[KC];
 #pragma unroll
         for (int i = 0; i < KC; ++i) {
           const int off = staps[q0 + i];
-          const float v = off >= 0 ? src[off] : 0.f;
+          const float v = off >= 0 ? src[off + shs[strow[q0 + i]]] : 0.f;
           float h, l;
           split_tf32(v, h, l);
           hi[i] = __float_as_uint(h);
@@ -332,8 +362,17 @@ bool direct_tc_enabled() {
 // k = 4: 16 unaligned rows by 4-byte LDGSTS, no reuse between neighbouring
 // rows), whatever the channel block: it beats the FFMA kernel from 48 maps
 // per launch on (80 maps: 6.3 vs 12.4 ms at 330^3), not below.
+int64_t direct_tc_min_maps() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("VXG_DIRECT_TC_MIN");
+    return e ? int64_t(std::atoll(e)) : int64_t(48);
+  }();
+  return v;
+}
+
 bool direct_tc_supported(int64_t f, int64_t fo, V3 k) {
-  return direct_tc_enabled() && f == 1 && fo % 16 == 0 && fo >= 48 && fo <= 80 && k.x * k.y <= DT_ROWS &&
+  return direct_tc_enabled() && f == 1 && fo % 16 == 0 && fo >= direct_tc_min_maps() && fo <= 80 &&
+         k.x * k.y <= DT_ROWS &&
          k.vol() <= 64 && TC_M + k.z - 1 <= DT_RS;
 }
 
@@ -352,6 +391,7 @@ void launch_direct_tc(Ctx* c, const float* in, i64 S, V3 n, const float* w, i64 
   g.ztiles = (g.oz + TC_M - 1) / TC_M;
   g.tiles = S * g.ox * g.oy * int64_t(g.ztiles);
   g.relu = relu ? 1 : 0;
+  g.vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0 ? 1 : 0;
   if (g.tiles == 0) return;
   const double vox = double(g.ox) * g.oy * g.oz;
   KScope ks(c, VXG_K_DIRECT, 2.0 * double(S) * fo * vox * double(g.kvol),
