@@ -9,7 +9,7 @@
 //
 // Persistent CTAs (one per SM), warp-specialised like the contraction:
 //   warps 0,2,3 producers: the kx*ky input row segments of a tile (128 + kz - 1
-//               floats each, zero past the image) into a 4-slot ring, by
+//               floats each, zero past the image) into a 8-slot ring, by
 //               16-byte cp.async of each segment's aligned superset (the
 //               row's misalignment recorded per slot) when the input is
 //               16-byte aligned, else 4-byte copies;
@@ -36,7 +36,7 @@ namespace {
 using namespace tc;
 
 constexpr int DT_THREADS = 384;
-constexpr int DT_NS = 4;     // staging slots
+constexpr int DT_NS = 8;     // staging slots
 constexpr int DT_RS = 136;   // staged row stride (floats): 128 + kz - 1 <= 136
 constexpr int DT_ROWS = 16;  // kx * ky <= 16
 
@@ -62,9 +62,9 @@ struct DtCfg {
   static constexpr int SLOT = DT_ROWS * DT_RS * 4;
   static constexpr int OFF_BIAS = 512;   // N floats
   static constexpr int OFF_TAPS = 1024;  // K ints: staged-row offset of tap q (-1: padding)
-  static constexpr int OFF_SHIFT = 1280; // [slot][row] ints: where a staged row's z0 lands (16-byte path)
-  static constexpr int OFF_TROW = 1536;  // K ints: staged row of tap q
-  static constexpr int OFF_W = 2048;
+  static constexpr int OFF_TROW = 1280;  // K ints: staged row of tap q
+  static constexpr int OFF_SHIFT = 1536; // [slot][row] ints: where a staged row's z0 lands (16-byte path)
+  static constexpr int OFF_W = 2048;  // (shift table: DT_NS x 16 ints = 512 B)
   static constexpr int OFF_RING = OFF_W + W_BYTES;
   static constexpr int SMEM = OFF_RING + DT_NS * SLOT;
   // more than half an SM's shared memory: one CTA per SM, so the 512-column
@@ -168,7 +168,18 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = *tmem_slot;
 
+  const bool small = g.tiles < (int64_t(1) << 31);
   auto decode = [&](int64_t lt, int64_t& s, int& x, int& y, int& z0) {
+    if (small) {  // 32-bit division (the 64-bit one is a long software sequence)
+      int t = int(blockIdx.x + lt * gridDim.x);
+      z0 = (t % g.ztiles) * TC_M;
+      t /= g.ztiles;
+      y = t % g.oy;
+      t /= g.oy;
+      x = t % g.ox;
+      s = t / g.ox;
+      return;
+    }
     int64_t t = blockIdx.x + lt * gridDim.x;
     z0 = int(t % g.ztiles) * TC_M;
     t /= g.ztiles;
