@@ -37,6 +37,7 @@ using namespace tc;
 
 constexpr int DT_THREADS = 384;
 constexpr int DT_NS = 8;     // staging slots
+constexpr int DT_DEPTH = 4;  // tiles of copies in flight per producer thread (< DT_NS)
 constexpr int DT_RS = 136;   // staged row stride (floats): 128 + kz - 1 <= 136
 constexpr int DT_ROWS = 16;  // kx * ky <= 16
 
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   }
   if (tid == 32) {
     for (int s = 0; s < DT_NS; ++s) {
-      mbar_init(&full[s], 96 + 3);  // 3 producer warps' cp.async arrivals + their shift-table arrives
+      mbar_init(&full[s], 96);  // every producer lane, once its copies of the tile landed
       mbar_init(&slot_empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
@@ -229,9 +230,18 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
           if (lane == 0) sshift[s * DT_ROWS + r] = 0;
         }
       }
-      cp_async_arrive_noinc(&full[s]);
-      if (lane == 0) mbar_arrive(&full[s]);  // releases this warp's shift-table entries
+      // per-tile completion: after committing tile lt, wait for tile lt - D
+      // and release it (a cp.async-tracked arrive only fires once ALL of the
+      // thread's outstanding copies are done, i.e. in bursts of a whole ring)
+      cp_async_commit();
+      if (lt >= DT_DEPTH) {
+        cp_async_wait<DT_DEPTH>();
+        mbar_arrive(&full[int((lt - DT_DEPTH) % DT_NS)]);
+      }
     }
+    cp_async_wait<0>();
+    for (int64_t lt = my_tiles > DT_DEPTH ? my_tiles - DT_DEPTH : 0; lt < my_tiles; ++lt)
+      mbar_arrive(&full[int(lt % DT_NS)]);
   } else if (warp >= 8) {
     // ---------------- converters: thread m owns output voxel z0 + m ----------------
     const int m = tid - 256;
