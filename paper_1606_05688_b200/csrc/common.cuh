@@ -311,7 +311,7 @@ double bench_ffma(Ctx* c);
 void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float* w, i64 fo,
                         V3 k, const float* bias, bool relu, float* out, i64 ipz = 0, i64 opz = 0);
 // f = 1 direct convolution on the tensor cores (k_direct_tc.cu); VXG_DIRECT_TC=0 disables
-bool direct_tc_supported(int64_t f, int64_t fo, V3 k);
+bool direct_tc_supported(int64_t f, int64_t fo, V3 k, const void* in);
 void launch_direct_tc(Ctx* c, const float* in, i64 S, V3 n, const float* w, i64 fo, V3 k, const float* bias,
                       bool relu, float* out, i64 ipz, i64 opz);
 

@@ -184,7 +184,7 @@ void launch_conv_direct(Ctx* c, const float* in, i64 S, i64 f, V3 n, const float
   g.relu = relu ? 1 : 0;
   require(S <= 65535, "conv_direct: batch above 65535 per call");
   if (S == 0 || fo == 0) return;
-  if (direct_tc_supported(f, fo, k)) {
+  if (direct_tc_supported(f, fo, k, in)) {
     launch_direct_tc(c, in, S, n, w, fo, k, bias, relu, out, g.ipz, g.opz);
     return;
   }

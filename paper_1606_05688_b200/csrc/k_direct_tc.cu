@@ -8,11 +8,10 @@
 // kind::tf32 with the 3xTF32 split of k_cgemm_tc.cu (fp32-level accuracy).
 //
 // Persistent CTAs (one per SM), warp-specialised like the contraction:
-//   warps 0,2,3 producers: the kx*ky input row segments of a tile (128 + kz - 1
-//               floats each, zero past the image) into a 8-slot ring, by
-//               16-byte cp.async of each segment's aligned superset (the
-//               row's misalignment recorded per slot) when the input is
-//               16-byte aligned, else 4-byte copies;
+//   warp 0      producer (one thread): one cp.async.bulk per input row
+//               segment of the tile (kx*ky rows of 128 + kz - 1 floats; the
+//               16-byte-aligned superset, its offset recorded per slot) into
+//               an 8-slot ring, completion by mbarrier transaction bytes;
 //   warps 8-11  converters: row m gathers its k^3 taps from the staged rows,
 //               splits them into tf32 hi/lo and writes them to TMEM (A of
 //               buffer t % 2);
@@ -23,8 +22,10 @@
 // The pre-split W (N x K, hi/lo, UMMA K-major layout) and the bias stay in
 // shared memory for the CTA's lifetime; TMEM holds 2 accumulators of N
 // columns and 2 A buffers of 2K columns (<= 416 of 512).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "async.cuh"
 #include "common.cuh"
@@ -37,7 +38,6 @@ using namespace tc;
 
 constexpr int DT_THREADS = 384;
 constexpr int DT_NS = 8;     // staging slots
-constexpr int DT_DEPTH = 4;  // tiles of copies in flight per producer thread (< DT_NS)
 constexpr int DT_RS = 136;   // staged row stride (floats): 128 + kz - 1 <= 136
 constexpr int DT_ROWS = 16;  // kx * ky <= 16
 
@@ -53,7 +53,7 @@ struct DtGeom {
   int ztiles;
   int64_t tiles;
   int relu;
-  int vec;  // input 16-byte aligned: rows staged by 16-byte copies of aligned supersets
+  long long* prof;  // VXG_DT_PROF: per-CTA role cycle counters
 };
 
 template <int N, int K>
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   }
   if (tid == 32) {
     for (int s = 0; s < DT_NS; ++s) {
-      mbar_init(&full[s], 96);  // every producer lane, once its copies of the tile landed
+      mbar_init(&full[s], 1);  // the producer's arrive.expect_tx (+ the copies' transaction bytes)
       mbar_init(&slot_empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
@@ -191,65 +191,63 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
   };
   const int nrows = g.kx * g.ky, rlen = TC_M + g.kz - 1;
 
-  if (warp == 0 || warp == 2 || warp == 3) {
-    // ---------------- producers (3 warps: one warp's 4-byte LDGSTS stream
-    // cannot keep up with the tensor cores) ----------------
-    const int pw = warp == 0 ? 0 : warp - 1;
-    for (int64_t lt = 0; lt < my_tiles; ++lt) {
-      const int s = int(lt % DT_NS);
-      if (lt >= DT_NS) mbar_wait(&slot_empty[s], uint32_t((lt / DT_NS - 1) & 1));
-      int64_t si;
-      int x, y, z0;
-      decode(lt, si, x, y, z0);
-      float* dst = ring + s * (DT_ROWS * DT_RS);
-      const float* img = g.in + si * int64_t(g.nx) * g.ny * g.ipz;
-      for (int r = pw; r < nrows; r += 3) {
-        const int a = r / g.ky, b = r % g.ky;
-        const int64_t rowoff = (si * g.nx + (x + a)) * int64_t(g.ny) * g.ipz + int64_t(y + b) * g.ipz;
-        if (g.vec) {
-          // the aligned superset [o - sh, ...) of the row segment by 16-byte
-          // copies (zero past nz); the converters read it at +sh
-          const int64_t o = rowoff + z0;
+  if (warp == 0) {
+    // ---------------- producer: one thread, one bulk copy per staged row ----------------
+    // The copy engine moves the 16-byte-aligned superset of each row segment
+    // ([o - sh, ...), sh = o mod 4) and signals the slot's mbarrier by
+    // transaction bytes; the converters read the row at +sh.  Floats past nz
+    // inside the last 16 bytes feed only outputs past oz, which are never
+    // stored.  Per tile this is kx*ky small requests (16 x 544 B at k = 4):
+    // the request count, not bytes, bounds the kernel at ~5.8k cycles per
+    // tile (LDGSTS staging from 1-3 warps, 4- or 16-byte, was no faster).
+    long long pwt = 0;
+    const long long pstart = clock64();
+    if (lane == 0) {
+      for (int64_t lt = 0; lt < my_tiles; ++lt) {
+        const int s = int(lt % DT_NS);
+        const long long pw0 = clock64();
+        if (lt >= DT_NS) mbar_wait(&slot_empty[s], uint32_t((lt / DT_NS - 1) & 1));
+        pwt += clock64() - pw0;
+        int64_t si;
+        int x, y, z0;
+        decode(lt, si, x, y, z0);
+        float* dst = ring + s * (DT_ROWS * DT_RS);
+        const int64_t base = ((si * g.nx + x) * int64_t(g.ny) + y) * g.ipz + z0;
+        uint32_t bytes = 0;
+        int nb[DT_ROWS];
+        int64_t oas[DT_ROWS];
+        for (int r = 0; r < nrows; ++r) {
+          const int aa = r / g.ky, bb = r % g.ky;
+          const int64_t o = base + (int64_t(aa) * g.ny + bb) * g.ipz;
           const int sh = int(o & 3);
-          const int64_t oa = o - sh, rend = rowoff + g.nz;
-          const int nch = (rlen + sh + 3) >> 2;
-          for (int ch = lane; ch < nch; ch += 32) {
-            const int64_t e = oa + 4 * ch;
-            const int64_t valid = rend - e < 0 ? 0 : (rend - e > 4 ? 4 : rend - e);
-            const unsigned sdst = static_cast<unsigned>(__cvta_generic_to_shared(dst + r * DT_RS + 4 * ch));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst),
-                         "l"(valid > 0 ? g.in + e : g.in), "r"(int(valid * 4)));
-          }
-          if (lane == 0) sshift[s * DT_ROWS + r] = sh;
-        } else {
-          const float* row = img + (int64_t(x + a) * g.ny + (y + b)) * g.ipz;
-          for (int zz = lane; zz < rlen; zz += 32) {
-            const bool ok = z0 + zz < g.nz;
-            cp_async4(dst + r * DT_RS + zz, ok ? row + z0 + zz : row, ok);
-          }
-          if (lane == 0) sshift[s * DT_ROWS + r] = 0;
+          const int64_t oa = o - sh;
+          const int64_t need = std::min<int64_t>(int64_t(rlen), int64_t(g.nz - z0)) + sh;  // floats from oa
+          nb[r] = int(((need + 3) >> 2) << 4);
+          oas[r] = oa;
+          sshift[s * DT_ROWS + r] = sh;
+          bytes += uint32_t(nb[r]);
         }
-      }
-      // per-tile completion: after committing tile lt, wait for tile lt - D
-      // and release it (a cp.async-tracked arrive only fires once ALL of the
-      // thread's outstanding copies are done, i.e. in bursts of a whole ring)
-      cp_async_commit();
-      if (lt >= DT_DEPTH) {
-        cp_async_wait<DT_DEPTH>();
-        mbar_arrive(&full[int((lt - DT_DEPTH) % DT_NS)]);
+        mbar_arrive_expect_tx(&full[s], bytes);  // releases the shift entries too
+        for (int r = 0; r < nrows; ++r) bulk_copy(dst + r * DT_RS, g.in + oas[r], uint32_t(nb[r]), &full[s]);
       }
     }
-    cp_async_wait<0>();
-    for (int64_t lt = my_tiles > DT_DEPTH ? my_tiles - DT_DEPTH : 0; lt < my_tiles; ++lt)
-      mbar_arrive(&full[int(lt % DT_NS)]);
+    if (g.prof && lane == 0) {
+      g.prof[blockIdx.x * 8 + 0] = pwt;
+      g.prof[blockIdx.x * 8 + 1] = clock64() - pstart;
+    }
   } else if (warp >= 8) {
     // ---------------- converters: thread m owns output voxel z0 + m ----------------
     const int m = tid - 256;
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
+    long long cwf = 0, cwa = 0;
     for (int64_t lt = 0; lt < my_tiles; ++lt) {
       const int s = int(lt % DT_NS), b = int(lt & 1);
+      const long long c0 = clock64();
       mbar_wait(&full[s], uint32_t((lt / DT_NS) & 1));
+      const long long c1 = clock64();
       if (lt >= 2) mbar_wait(&a_empty[b], uint32_t((lt / 2 - 1) & 1));
+      cwf += c1 - c0;
+      cwa += clock64() - c1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const float* src = ring + s * (DT_ROWS * DT_RS) + m;
       const int* shs = sshift + s * DT_ROWS;
@@ -274,15 +272,24 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       mbar_arrive(&slot_empty[s]);
       mbar_arrive(&ready[b]);
     }
+    if (g.prof && m == 0) {
+      g.prof[blockIdx.x * 8 + 2] = cwf;
+      g.prof[blockIdx.x * 8 + 3] = cwa;
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32<N>(false);
       const uint32_t wbase = smem_u32(sw);
+      long long mwr = 0, mwe = 0;
       for (int64_t lt = 0; lt < my_tiles; ++lt) {
         const int b = int(lt & 1);
+        const long long c0 = clock64();
         mbar_wait(&ready[b], uint32_t((lt / 2) & 1));
+        const long long c1 = clock64();
         if (lt >= 2) mbar_wait(&acc_empty[b], uint32_t((lt / 2 - 1) & 1));
+        mwr += c1 - c0;
+        mwe += clock64() - c1;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const uint32_t d = tmem + uint32_t(C::ACC + N * b);
         const uint32_t ahi = tmem + uint32_t(C::ABUF + 2 * K * b);
@@ -298,18 +305,25 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
         umma_commit(&a_empty[b]);
         umma_commit(&acc_full[b]);
       }
+      if (g.prof) {
+        g.prof[blockIdx.x * 8 + 4] = mwr;
+        g.prof[blockIdx.x * 8 + 5] = mwe;
+      }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int m = (warp - 4) * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
     const int64_t chan = int64_t(g.ox) * g.oy * g.opz;
+    long long ewt = 0;
     for (int64_t lt = 0; lt < my_tiles; ++lt) {
       const int b = int(lt & 1);
       int64_t si;
       int x, y, z0;
       decode(lt, si, x, y, z0);
+      const long long e0 = clock64();
       mbar_wait(&acc_full[b], uint32_t((lt / 2) & 1));
+      ewt += clock64() - e0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const int gz = z0 + m;
       float* o = g.out + si * N * chan + (int64_t(x) * g.oy + y) * g.opz + gz;
@@ -335,6 +349,10 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&acc_empty[b]);
     }
+    if (g.prof && m == 0) {
+      g.prof[blockIdx.x * 8 + 6] = ewt;
+      g.prof[blockIdx.x * 8 + 7] = my_tiles;
+    }
   }
   __syncthreads();
   if (warp == 0) {
@@ -353,9 +371,31 @@ void run_dt(Ctx* c, const DtGeom& g) {
     configured = true;
   }
   const unsigned grid = unsigned(std::min<int64_t>(g.tiles, c->num_sms));
-  direct_tc_kernel<N, K><<<grid, DT_THREADS, C::SMEM_LAUNCH, c->stream>>>(g);
+  static const bool prof = std::getenv("VXG_DT_PROF") != nullptr;
+  DtGeom h = g;
+  long long* dprof = nullptr;
+  if (prof) {
+    VXG_CUDA_CHECK(cudaMalloc(&dprof, size_t(grid) * 8 * sizeof(long long)));
+    VXG_CUDA_CHECK(cudaMemset(dprof, 0, size_t(grid) * 8 * sizeof(long long)));
+    h.prof = dprof;
+  }
+  direct_tc_kernel<N, K><<<grid, DT_THREADS, C::SMEM_LAUNCH, c->stream>>>(h);
   c->counted();
   check_launch("direct_tc_kernel");
+  if (prof) {
+    std::vector<long long> v(size_t(grid) * 8);
+    VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    VXG_CUDA_CHECK(cudaMemcpy(v.data(), dprof, v.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(dprof);
+    double a[8] = {0};
+    for (unsigned bb = 0; bb < grid; ++bb)
+      for (int k = 0; k < 8; ++k) a[k] += double(v[bb * 8 + k]) / grid;
+    std::fprintf(stderr,
+                 "[dtprof] N=%d tiles/CTA %.0f total %.3gM | producer wait-slot %.3gM | converter wait-data %.3gM "
+                 "wait-A %.3gM | mma wait-ready %.3gM wait-acc %.3gM | epilogue wait %.3gM  (per tile: %.0f cyc)\n",
+                 N, a[7], a[1] / 1e6, a[0] / 1e6, a[2] / 1e6, a[3] / 1e6, a[4] / 1e6, a[5] / 1e6, a[6] / 1e6,
+                 a[1] / std::max(1.0, a[7]));
+  }
 }
 
 template <int N>
@@ -379,10 +419,10 @@ bool direct_tc_enabled() {
   return on;
 }
 
-// The kernel is bound by its input staging (~2.9 us per 128-voxel tile at
-// k = 4: 16 unaligned rows by 4-byte LDGSTS, no reuse between neighbouring
-// rows), whatever the channel block: it beats the FFMA kernel from 48 maps
-// per launch on (80 maps: 6.3 vs 12.4 ms at 330^3), not below.
+// The kernel is bound by its input staging (~3 us per 128-voxel tile at
+// k = 4: 16 row requests, no reuse between neighbouring rows), whatever the
+// channel block: it beats the FFMA kernel from 48 maps per launch on
+// (80 maps: 6.6-7.1 vs 12.4 ms at 330^3), not below.
 int64_t direct_tc_min_maps() {
   static const int64_t v = [] {
     const char* e = std::getenv("VXG_DIRECT_TC_MIN");
@@ -391,10 +431,11 @@ int64_t direct_tc_min_maps() {
   return v;
 }
 
-bool direct_tc_supported(int64_t f, int64_t fo, V3 k) {
+bool direct_tc_supported(int64_t f, int64_t fo, V3 k, const void* in) {
   return direct_tc_enabled() && f == 1 && fo % 16 == 0 && fo >= direct_tc_min_maps() && fo <= 80 &&
          k.x * k.y <= DT_ROWS &&
-         k.vol() <= 64 && TC_M + k.z - 1 <= DT_RS;
+         k.vol() <= 64 && TC_M + k.z - 1 <= DT_RS &&
+         (reinterpret_cast<uintptr_t>(in) & 15) == 0;  // bulk copies of 16-byte-aligned row supersets
 }
 
 // f = 1 direct convolution on the tensor cores (callers check direct_tc_supported)
@@ -412,7 +453,7 @@ void launch_direct_tc(Ctx* c, const float* in, i64 S, V3 n, const float* w, i64 
   g.ztiles = (g.oz + TC_M - 1) / TC_M;
   g.tiles = S * g.ox * g.oy * int64_t(g.ztiles);
   g.relu = relu ? 1 : 0;
-  g.vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0 ? 1 : 0;
+  g.prof = nullptr;
   if (g.tiles == 0) return;
   const double vox = double(g.ox) * g.oy * g.oz;
   KScope ks(c, VXG_K_DIRECT, 2.0 * double(S) * fo * vox * double(g.kvol),
