@@ -296,8 +296,10 @@ inline void check_launch(const char* what) {
 // MPF of S whole entries (all P fragments); the output may be the channel
 // slice [c0, c0+f) of a tensor with f_tot channels (f_tot <= 0: f)
 // ipz / opz: z row pitch of input / output (0: unpadded)
+// mx_out / x_out0: the pooled fragments of an x slab of the input go to x
+// positions [x_out0, x_out0 + n.x / 2) of fragments mx_out wide (2x2x2 only)
 void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot = 0,
-                i64 c0 = 0, i64 ipz = 0, i64 opz = 0);
+                i64 c0 = 0, i64 ipz = 0, i64 opz = 0, i64 mx_out = 0, i64 x_out0 = 0);
 void launch_maxpool(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out);
 void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
                       const i64* windows, int nwin, float* dense, i64 S0, i64 fpz = 0);

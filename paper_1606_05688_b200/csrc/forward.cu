@@ -32,6 +32,16 @@ int64_t entry_bytes(const ForwardPlan& p, size_t li) {
   return s.f * s.n.x * s.n.y * p.pz[li] * 4;
 }
 
+// VXG_SLAB_FUSION=0: fuse a first direct layer with its MPF by channel blocks
+// instead of x slabs (A/B timing)
+bool slab_fusion() {
+  static const bool on = [] {
+    const char* e = std::getenv("VXG_SLAB_FUSION");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
 }  // namespace
 
 Model::Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr) : c(ctx), net(n) {
@@ -327,11 +337,42 @@ struct Runner {
     const Layer& l = m.net.layers[li];
     const Shape& si = p.shapes[li];
     if (st.fused) {
-      // direct conv one channel block at a time, each block pooled straight
-      // into its channel slice of the MPF output
       const Layer& pool = m.net.layers[li + 1];
       const Shape& mid = p.shapes[li + 1];
       const int ci = m.conv_index[li];
+      // single input map and 2x2x2 windows: x slabs of the conv output with
+      // every output map (so the tensor-core direct kernel sees all f' maps),
+      // each slab pooled into its x range of the fragments.  A slab of xs
+      // (odd) conv planes yields (xs - 1) / 2 pooled planes for all 8
+      // offsets; consecutive slabs share one conv plane.
+      const int64_t plane_bytes = mid.f * mid.n.y * p.pz[li + 1] * 4;  // one conv x plane, all maps
+      int64_t xs = avail() / std::max<int64_t>(plane_bytes, 1);
+      xs = std::min(xs, mid.n.x);
+      if (xs % 2 == 0) xs -= 1;
+      if (si.f == 1 && pool.ext.x == 2 && pool.ext.y == 2 && pool.ext.z == 2 && xs >= 3 && slab_fusion()) {
+        DevBuf tmp(m.c, xs * plane_bytes);
+        const int64_t mx_full = mid.n.x / 2;
+        const V3 n_in = si.n;
+        const int64_t in_entry = n_in.x * n_in.y * p.pz[li];                  // f = 1
+        const int64_t out_entry = int64_t(pool.ext.vol()) * l.fo * mx_full * (mid.n.y / 2) * p.pz[li + 2];
+        for (int64_t e = 0; e < g; ++e) {
+          for (int64_t x0 = 0; x0 + 1 < mid.n.x; x0 += xs - 1) {
+            const int64_t nxs = std::min(xs, mid.n.x - x0);  // odd: x0 even, mid.n.x odd
+            int h = timer.begin(li);
+            conv_direct_device(m.c, in + e * in_entry + x0 * n_in.y * p.pz[li], 1, 1,
+                               V3{nxs + l.ext.x - 1, n_in.y, n_in.z}, m.kern[size_t(ci)].as<float>(), l.fo, l.ext,
+                               m.bias[size_t(ci)].as<float>(), l.relu, tmp.as<float>(), p.pz[li], p.pz[li + 1]);
+            timer.end(h);
+            h = timer.begin(li + 1);
+            launch_mpf(m.c, tmp.as<float>(), 1, l.fo, V3{nxs, mid.n.y, mid.n.z}, pool.ext, dst + e * out_entry, l.fo,
+                       0, p.pz[li + 1], p.pz[li + 2], mx_full, x0 / 2);
+            timer.end(h);
+          }
+        }
+        return;
+      }
+      // otherwise direct conv one channel block at a time, each block pooled
+      // straight into its channel slice of the MPF output
       const int64_t per_ch = g * mid.n.x * mid.n.y * p.pz[li + 1] * 4;
       int64_t cb = std::max<int64_t>(1, avail() / std::max<int64_t>(per_ch, 1));
       cb = std::min(cb, l.fo);
@@ -626,12 +667,16 @@ void Model::tune(int64_t S, V3 e) {
         const V3 ns{d + k.x - 1, d + k.y - 1, d + k.z - 1};
         DevBuf x(c, f * ns.vol() * 4), y(c, fo * d * d * d * 4);
         fill_sample(c, x.as<float>(), f * ns.vol(), 777u);
-        // followed by an MPF, the forward fuses the two by channel blocks whose
-        // width the free memory sets (16 at the big patches the planner is for);
-        // time that block width, since the kernel choice depends on it
+        // followed by an MPF, the forward fuses the two: by x slabs with every
+        // map (single input map, 2x2x2 windows), else by channel blocks whose
+        // width the free memory sets (16 at the big patches the planner is
+        // for); time the width the forward will use, since the kernel choice
+        // depends on it
         const bool fused = li + 1 < p0.shapes.size() - 1 && net.layers[li + 1].kind == 1 &&
                            p0.pool_mode[li + 1] == 1;
-        const int64_t cb = fused ? std::min<int64_t>(16, fo) : fo;
+        const V3 pw = fused ? net.layers[li + 1].ext : V3{0, 0, 0};
+        const bool slabs = fused && f == 1 && pw.x == 2 && pw.y == 2 && pw.z == 2 && slab_fusion();
+        const int64_t cb = fused && !slabs ? std::min<int64_t>(16, fo) : fo;
         const double t = time_on_stream(c, [&] {
           for (int64_t c0 = 0; c0 < fo; c0 += cb)
             conv_direct_device(c, x.as<float>(), 1, f, ns, w + c0 * f * k.vol(), std::min(cb, fo - c0), k,

@@ -112,6 +112,7 @@ struct MpfGeom {
   int tiles_z, tiles_y, tiles_x;
   int64_t planes;       // S * f
   int ipz, opz;         // z row pitch of input / output planes
+  int mx_out, x_out0;   // output fragment x extent and x offset (x-slab pooling; mpf222 only)
 };
 
 constexpr int MPF_TZ = 32, MPF_TY = 8, MPF_XT = 16;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
   const int x1 = min(M2_XT, g.dx - x0);
   const bool live = z < g.dz && y < g.dy;    // dz is even: z + 1 < dz too
   const int64_t nel = int64_t(g.nx) * g.ny * g.ipz;
-  const int moel = g.mx * g.my * g.opz;
+  const int moel = g.mx_out * g.my * g.opz;
   const int64_t fstride = int64_t(g.f_tot) * moel;
   const int offy = (y & 1) * 2;
   const bool vec = (g.ipz & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     const int64_t mstep = int64_t(g.my) * g.opz;  // one fragment x row
     // fragment pointers for D row parity (x even / odd) and column parity
     float* q0 = out + ((s * g.P) * g.f_tot + g.c0 + fm) * int64_t(moel) + int64_t(y >> 1) * g.opz +
-                (z >> 1) + int64_t(x0 >> 1) * mstep;
+                (z >> 1) + int64_t((x0 >> 1) + g.x_out0) * mstep;
     float* qe0 = q0 + int64_t(0 + offy) * fstride;
     float* qe1 = q0 + int64_t(1 + offy) * fstride;
     float* qo0 = q0 + int64_t(4 + offy) * fstride;
@@ -401,11 +402,16 @@ __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict_
 }  // namespace
 
 void launch_mpf(Ctx* c, const float* in, i64 S, i64 f, V3 n, V3 p, float* out, i64 f_tot,
-                i64 c0, i64 ipz, i64 opz) {
+                i64 c0, i64 ipz, i64 opz, i64 mx_out, i64 x_out0) {
   require(p.x <= 8, "mpf: window above 8 along x");
   MpfGeom g{};
   g.nx = int(n.x); g.ny = int(n.y); g.nz = int(n.z);
   g.mx = int(n.x / p.x); g.my = int(n.y / p.y); g.mz = int(n.z / p.z);
+  g.mx_out = int(mx_out > 0 ? mx_out : g.mx);
+  g.x_out0 = int(x_out0);
+  require((g.mx_out == g.mx && g.x_out0 == 0) || (p.x == 2 && p.y == 2 && p.z == 2),
+          "mpf: x-slab pooling is implemented for 2x2x2 windows only");
+  require(g.x_out0 + g.mx <= g.mx_out, "mpf: x slab outside the output");
   g.px = int(p.x); g.py = int(p.y); g.pz = int(p.z); g.P = int(p.vol());
   g.dx = g.px * g.mx; g.dy = g.py * g.my; g.dz = g.pz * g.mz;
   g.f = int(f);
