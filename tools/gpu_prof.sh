@@ -14,6 +14,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"cgemm_tc_kernel|tile_fwd_pair_kernel|tile_inv_pair_kernel" --launch-skip 3 --launch-count 3 \
   -o gpurun_out/${TAG}_layer -f python tools/kbench.py --which conv --S 64 --n 85 > gpurun_out/${TAG}_ncu_layer.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"mpf222_kernel|conv_direct_kernel" --launch-skip 1 --launch-count 3 \
+  -k regex:"mpf222_kernel|conv_direct_kernel|direct_tc_kernel" --launch-skip 1 --launch-count 3 \
   -o gpurun_out/${TAG}_small -f python tools/kbench.py --which direct,mpf --n 85 > gpurun_out/${TAG}_ncu_small.log 2>&1
 ls -la gpurun_out
