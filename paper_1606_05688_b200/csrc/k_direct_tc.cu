@@ -8,7 +8,7 @@
 // kind::tf32 with the 3xTF32 split of k_cgemm_tc.cu (fp32-level accuracy).
 //
 // Persistent CTAs (one per SM), warp-specialised like the contraction:
-//   warp 0      producer (one thread): one cp.async.bulk per input row
+//   warp 0      producer (lane r: row r): one cp.async.bulk per input row
 //               segment of the tile (kx*ky rows of 128 + kz - 1 floats; the
 //               16-byte-aligned superset, its offset recorded per slot) into
 //               an 8-slot ring, completion by mbarrier transaction bytes;
@@ -197,39 +197,38 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
     // ([o - sh, ...), sh = o mod 4) and signals the slot's mbarrier by
     // transaction bytes; the converters read the row at +sh.  Floats past nz
     // inside the last 16 bytes feed only outputs past oz, which are never
-    // stored.  Per tile this is kx*ky small requests (16 x 544 B at k = 4):
-    // the request count, not bytes, bounds the kernel at ~5.8k cycles per
-    // tile (LDGSTS staging from 1-3 warps, 4- or 16-byte, was no faster).
+    // stored.
     long long pwt = 0;
     const long long pstart = clock64();
-    if (lane == 0) {
-      for (int64_t lt = 0; lt < my_tiles; ++lt) {
-        const int s = int(lt % DT_NS);
-        const long long pw0 = clock64();
-        if (lt >= DT_NS) mbar_wait(&slot_empty[s], uint32_t((lt / DT_NS - 1) & 1));
-        pwt += clock64() - pw0;
-        int64_t si;
-        int x, y, z0;
-        decode(lt, si, x, y, z0);
-        float* dst = ring + s * (DT_ROWS * DT_RS);
-        const int64_t base = ((si * g.nx + x) * int64_t(g.ny) + y) * g.ipz + z0;
-        uint32_t bytes = 0;
-        int nb[DT_ROWS];
-        int64_t oas[DT_ROWS];
-        for (int r = 0; r < nrows; ++r) {
-          const int aa = r / g.ky, bb = r % g.ky;
-          const int64_t o = base + (int64_t(aa) * g.ny + bb) * g.ipz;
-          const int sh = int(o & 3);
-          const int64_t oa = o - sh;
-          const int64_t need = std::min<int64_t>(int64_t(rlen), int64_t(g.nz - z0)) + sh;  // floats from oa
-          nb[r] = int(((need + 3) >> 2) << 4);
-          oas[r] = oa;
-          sshift[s * DT_ROWS + r] = sh;
-          bytes += uint32_t(nb[r]);
-        }
-        mbar_arrive_expect_tx(&full[s], bytes);  // releases the shift entries too
-        for (int r = 0; r < nrows; ++r) bulk_copy(dst + r * DT_RS, g.in + oas[r], uint32_t(nb[r]), &full[s]);
-      }
+    // lane r < kx*ky owns staged row r: the row requests of a tile are issued
+    // by different threads in parallel (one thread issuing all 16 in turn
+    // was the kernel's bound)
+    const int r = lane;
+    const int aa = r < nrows ? r / g.ky : 0, bb = r < nrows ? r % g.ky : 0;
+    const int64_t roff = (int64_t(aa) * g.ny + bb) * g.ipz;
+    for (int64_t lt = 0; lt < my_tiles; ++lt) {
+      const int s = int(lt % DT_NS);
+      const long long pw0 = clock64();
+      if (lt >= DT_NS) mbar_wait(&slot_empty[s], uint32_t((lt / DT_NS - 1) & 1));
+      pwt += clock64() - pw0;
+      int64_t si;
+      int x, y, z0;
+      decode(lt, si, x, y, z0);
+      float* dst = ring + s * (DT_ROWS * DT_RS);
+      const int64_t o = ((si * g.nx + x) * int64_t(g.ny) + y) * g.ipz + z0 + roff;
+      const int sh = int(o & 3);
+      const int64_t oa = o - sh;
+      const int64_t need = std::min<int64_t>(int64_t(rlen), int64_t(g.nz - z0)) + sh;  // floats from oa
+      const uint32_t nb = r < nrows ? uint32_t(((need + 3) >> 2) << 4) : 0u;
+      if (r < nrows) sshift[s * DT_ROWS + r] = sh;
+      // total bytes of the tile's rows (lanes >= nrows contribute 0)
+      uint32_t bytes = nb;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, d);
+      __syncwarp();  // orders the shift entries before lane 0's releasing arrive
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      __syncwarp();
+      if (r < nrows) bulk_copy(dst + r * DT_RS, g.in + oa, nb, &full[s]);
     }
     if (g.prof && lane == 0) {
       g.prof[blockIdx.x * 8 + 0] = pwt;
