@@ -16,7 +16,8 @@
 //               splits them into tf32 hi/lo and writes them to TMEM (A of
 //               buffer t % 2);
 //   warp 1      MMA issuer: 3 * K/8 MMAs into accumulator buffer t % 2;
-//   warps 4-7   epilogue: tcgen05.ld, bias + ReLU, stores -- lane m writes
+//   warps 4-7,  epilogue, one warpgroup per accumulator buffer: tcgen05.ld,
+//   12-15       bias + ReLU, stores -- lane m writes
 //               voxel z0 + m of each map, so every store instruction writes a
 //               whole 128-byte row segment (unlike the contraction's pieces).
 // The pre-split W (N x K, hi/lo, UMMA K-major layout) and the bias stay in
@@ -36,7 +37,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int DT_THREADS = 384;
+constexpr int DT_THREADS = 512;  // 16 warps: two epilogue warpgroups
 constexpr int DT_NS = 8;     // staging slots
 constexpr int DT_RS = 136;   // staged row stride (floats): 128 + kz - 1 <= 136
 constexpr int DT_ROWS = 16;  // kx * ky <= 16
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       g.prof[blockIdx.x * 8 + 0] = pwt;
       g.prof[blockIdx.x * 8 + 1] = clock64() - pstart;
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ---------------- converters: thread m owns output voxel z0 + m ----------------
     const int m = tid - 256;
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
@@ -310,13 +311,15 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue ----------------
-    const int m = (warp - 4) * 32 + lane;
+    // ---------------- epilogue: warps 4-7 drain accumulator 0 (even tiles),
+    // warps 12-15 accumulator 1 (odd tiles) ----------------
+    const int eg = warp >= 12 ? 1 : 0;
+    const int m = (warp & 3) * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
     const int64_t chan = int64_t(g.ox) * g.oy * g.opz;
     long long ewt = 0;
-    for (int64_t lt = 0; lt < my_tiles; ++lt) {
-      const int b = int(lt & 1);
+    for (int64_t lt = eg; lt < my_tiles; lt += 2) {
+      const int b = eg;
       int64_t si;
       int x, y, z0;
       decode(lt, si, x, y, z0);
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&acc_empty[b]);
     }
-    if (g.prof && m == 0) {
+    if (g.prof && m == 0 && eg == 0) {
       g.prof[blockIdx.x * 8 + 6] = ewt;
       g.prof[blockIdx.x * 8 + 7] = my_tiles;
     }
