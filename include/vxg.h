@@ -202,7 +202,8 @@ int vxg_net_forward(vxg_ctx* ctx, const vxg_net* net, const float* weights, int 
                     float* dense_out, vxg_report* report);
 
 /* Device-resident weights for repeated forwards (kernel spectra cached per
- * layer and FFT tile size, the "kernel-spectrum cache" of SURVEY 8f). */
+ * layer and FFT tile size, the "kernel-spectrum cache" of SURVEY 8f).
+ * weights == NULL creates a planning-only model (plan queries only). */
 typedef struct vxg_model vxg_model;
 int vxg_model_create(vxg_ctx* ctx, const vxg_net* net, const float* weights, int mem,
                      vxg_model** out);
@@ -211,6 +212,25 @@ int vxg_model_free(vxg_model* model);
 int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S,
                       const int64_t e[3], const int* conv_algos, int cache_spectra,
                       float* dense_out, vxg_report* report);
+
+/* vxg_model_forward with the pooling realisation chosen per pool layer, as an
+ * ExecutionPlan does (planner.hpp:94-125; PrimitiveKind pool_plain /
+ * pool_fragments): pool_modes holds one entry per pool layer, 0 = max_pool
+ * (plain), 1 = mpf_pool (fragments), NULL = the network's forced modes with
+ * fragments where it leaves the choice.  A mode contradicting a forced one is
+ * VXG_INVALID (planner.cpp:565-566).  dense_out has the plan's output shape:
+ * fragment pools are recombined, plain pools subsample. */
+int vxg_model_forward_ex(vxg_model* model, int mem, const float* input, int64_t S,
+                         const int64_t e[3], const int* conv_algos, const int* pool_modes,
+                         int cache_spectra, float* dense_out, vxg_report* report);
+
+/* The device plan for (S, e) with explicit pool modes: per layer 8 int64
+ * {kind (0 conv, 1 pool), conv algo or pool mode, tile T, tiles per entry,
+ * tensor cores, measured, estimated ns, 0} into out (8 * layers; may be NULL),
+ * and the peak HBM bytes of the forward into *bytes (may be NULL).  Works on a
+ * planning-only model (vxg_model_create with weights == NULL). */
+int vxg_model_plan_ex(vxg_model* model, int64_t S, const int64_t e[3], const int* conv_algos,
+                      const int* pool_modes, int64_t* out, int64_t* bytes);
 
 /* Streaming forward over `count` patches of the same shape (the tiler's
  * production path): double-buffered device tensors and two copy streams, so

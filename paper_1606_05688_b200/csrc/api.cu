@@ -13,9 +13,30 @@ using namespace vxg;
 namespace {
 
 thread_local std::string g_err;
+// device that was current when an entry point switched to its context's
+// device (-1: none); guard() switches back on the way out
+thread_local int g_prev_device = -1;
+
+void use_device(int device) {
+  int cur = 0;
+  VXG_CUDA_CHECK(cudaGetDevice(&cur));
+  if (cur == device) return;
+  if (g_prev_device < 0) g_prev_device = cur;
+  VXG_CUDA_CHECK(cudaSetDevice(device));
+}
+
+struct RestoreDevice {
+  ~RestoreDevice() {
+    if (g_prev_device >= 0) {
+      cudaSetDevice(g_prev_device);
+      g_prev_device = -1;
+    }
+  }
+};
 
 template <class F>
 int guard(F&& f) {
+  RestoreDevice restore;
   try {
     f();
     return VXG_OK;
@@ -44,9 +65,13 @@ void need(const void* p, const char* what) {
   if (!p) throw invalid(std::string(what) + ": null pointer");
 }
 
+// every entry point reaches its context through here: launches, streams and
+// allocations then target the context's device whatever the thread's current one
 Ctx* ctx_of(vxg_ctx* c) {
   if (!c) throw invalid("null context");
-  return reinterpret_cast<Ctx*>(c);
+  Ctx* x = reinterpret_cast<Ctx*>(c);
+  use_device(x->device);
+  return x;
 }
 
 // Input view: a device pointer, staged from host when needed.
@@ -636,8 +661,7 @@ int vxg_model_create(vxg_ctx* ctx, const vxg_net* net, const float* weights, int
   return guard([&] {
     Ctx* c = ctx_of(ctx);
     need(net, "vxg_model_create: net");
-    need(weights, "vxg_model_create: weights");
-    need(out, "vxg_model_create: out");
+    need(out, "vxg_model_create: out");  // weights == NULL: planning-only model
     auto* m = new vxg_model();
     try {
       m->m = std::make_unique<Model>(c, net->net, weights, mem == VXG_MEM_DEVICE);
@@ -652,6 +676,7 @@ int vxg_model_create(vxg_ctx* ctx, const vxg_net* net, const float* weights, int
 int vxg_model_free(vxg_model* model) {
   return guard([&] {
     if (model) {
+      use_device(model->m->c->device);
       cudaStreamSynchronize(model->m->c->stream);
       delete model;
     }
@@ -661,14 +686,22 @@ int vxg_model_free(vxg_model* model) {
 int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S, const int64_t e_[3],
                       const int* conv_algos, int cache_spectra, float* dense_out,
                       vxg_report* report) {
+  return vxg_model_forward_ex(model, mem, input, S, e_, conv_algos, nullptr, cache_spectra, dense_out,
+                              report);
+}
+
+int vxg_model_forward_ex(vxg_model* model, int mem, const float* input, int64_t S, const int64_t e_[3],
+                         const int* conv_algos, const int* pool_modes, int cache_spectra,
+                         float* dense_out, vxg_report* report) {
   return guard([&] {
     need(model, "vxg_model_forward: model");
+    use_device(model->m->c->device);
     need(input, "vxg_model_forward: input");
     need(dense_out, "vxg_model_forward: dense_out");
     Model& m = *model->m;
     Ctx* c = m.c;
     const V3 e = v3_checked(e_, "vxg_model_forward: e");
-    const ForwardPlan p = m.plan(S, e, conv_algos);
+    const ForwardPlan p = m.plan(S, e, conv_algos, pool_modes);
     AuditScope au(c);
     cudaEvent_t t0, t1;
     VXG_CUDA_CHECK(cudaEventCreate(&t0));
@@ -677,10 +710,13 @@ int vxg_model_forward(vxg_model* model, int mem, const float* input, int64_t S, 
     In xin(c, mem, input, S * m.net.fin * e.vol());
     Out o(c, mem, dense_out, S * p.f_out * p.dense.vol());
     std::vector<double> layer_s;
+    clear_flag_async(c);
     m.forward(p, xin.p, o.p, cache_spectra != 0, report ? &layer_s : nullptr);
     o.finish(c);
     VXG_CUDA_CHECK(cudaEventRecord(t1, c->stream));
     VXG_CUDA_CHECK(cudaEventSynchronize(t1));
+    // the pools of the forward scan their inputs (check_no_nan, layers.hpp:111-116)
+    if (read_and_clear_flag(c)) throw invalid("mpf_pool: NaN input rejected");
     float ms = 0;
     VXG_CUDA_CHECK(cudaEventElapsedTime(&ms, t0, t1));
     cudaEventDestroy(t0);
@@ -702,6 +738,7 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
                            float* const* outputs, double* seconds) {
   return guard([&] {
     need(model, "vxg_model_forward_many: model");
+    use_device(model->m->c->device);
     require(count >= 0, "vxg_model_forward_many: count must be >= 0");
     need(inputs, "vxg_model_forward_many: inputs");
     need(outputs, "vxg_model_forward_many: outputs");
@@ -756,6 +793,7 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
       VXG_CUDA_CHECK(cudaMemcpyAsync(din[b].get(), inputs[k], size_t(nin) * 4, cudaMemcpyHostToDevice, st.in));
       VXG_CUDA_CHECK(cudaEventRecord(h2d_done[b], st.in));
     };
+    clear_flag_async(c);
     if (count > 0) h2d(0);
     for (int64_t k = 0; k < count; ++k) {
       const int b = int(k % nbuf);
@@ -778,12 +816,14 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     if (seconds) *seconds = ms * 1e-3;
+    if (read_and_clear_flag(c)) throw invalid("mpf_pool: NaN input rejected");
   });
 }
 
 int vxg_model_tune(vxg_model* model, int64_t S, const int64_t e[3]) {
   return guard([&] {
     need(model, "vxg_model_tune: model");
+    use_device(model->m->c->device);
     model->m->tune(S, v3_checked(e, "vxg_model_tune: e"));
   });
 }
@@ -792,6 +832,7 @@ int vxg_model_plan_info(vxg_model* model, int64_t S, const int64_t e[3], const i
                         int64_t* out) {
   return guard([&] {
     need(model, "vxg_model_plan_info: model");
+    use_device(model->m->c->device);
     need(out, "vxg_model_plan_info: out");
     const ForwardPlan p = model->m->plan(S, v3_checked(e, "vxg_model_plan_info: e"), conv_algos);
     for (size_t li = 0; li < model->m->net.layers.size(); ++li) {
@@ -810,10 +851,37 @@ int vxg_model_plan_info(vxg_model* model, int64_t S, const int64_t e[3], const i
   });
 }
 
+int vxg_model_plan_ex(vxg_model* model, int64_t S, const int64_t e[3], const int* conv_algos,
+                      const int* pool_modes, int64_t* out, int64_t* bytes) {
+  return guard([&] {
+    need(model, "vxg_model_plan_ex: model");
+    use_device(model->m->c->device);
+    const Model& m = *model->m;
+    const ForwardPlan p = m.plan(S, v3_checked(e, "vxg_model_plan_ex: e"), conv_algos, pool_modes);
+    if (out)
+      for (size_t li = 0; li < m.net.layers.size(); ++li) {
+        const bool conv = m.net.layers[li].kind == 0;
+        const LayerChoice& ch = p.choice[li];
+        const bool fft = conv && ch.algo == VXG_CONV_FFT;
+        int64_t* o = out + 8 * li;
+        o[0] = conv ? 0 : 1;
+        o[1] = conv ? ch.algo : p.pool_mode[li];
+        o[2] = fft ? ch.fft.T : 0;
+        o[3] = fft ? ch.fft.tiles : 0;
+        o[4] = fft && ch.fft.tc ? 1 : 0;
+        o[5] = ch.measured ? 1 : 0;
+        o[6] = int64_t(ch.seconds * 1e9);
+        o[7] = 0;
+      }
+    if (bytes) *bytes = m.plan_bytes(p, true);
+  });
+}
+
 int64_t vxg_model_plan_bytes(vxg_model* model, int64_t S, const int64_t e[3], const int* algos) {
   int64_t r = -1;
   const int st = guard([&] {
     need(model, "vxg_model_plan_bytes");
+    use_device(model->m->c->device);
     const ForwardPlan p = model->m->plan(S, V3::of(e), algos);
     r = model->m->plan_bytes(p, true);
   });

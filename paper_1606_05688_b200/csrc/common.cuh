@@ -120,6 +120,18 @@ struct Arena {
   }
 };
 
+// One-time setup per device (kernel attributes such as the dynamic shared
+// memory limit are per device): first() is true once for each device.
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> mask{0};
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    return !(mask.fetch_or(b) & b);
+  }
+};
+
 // One context per GPU.  All work is issued on `stream`; allocations are
 // stream-ordered (cudaMallocAsync) and charged against `budget` bytes.
 struct Ctx {
@@ -305,6 +317,7 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
                       const i64* windows, int nwin, float* dense, i64 S0, i64 fpz = 0);
 void launch_nan_check(Ctx* c, const float* x, i64 count);
 bool read_and_clear_flag(Ctx* c);
+void clear_flag_async(Ctx* c);
 
 // instrumentation (k_misc.cu)
 double bench_ffma(Ctx* c);

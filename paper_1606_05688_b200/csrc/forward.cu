@@ -46,6 +46,7 @@ bool slab_fusion() {
 
 Model::Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr) : c(ctx), net(n) {
   net.validate();
+  has_weights = weights != nullptr;
   int64_t f = net.fin, off = 0;
   int ci = 0;
   for (const auto& l : net.layers) {
@@ -54,6 +55,10 @@ Model::Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr) : c(
       continue;
     }
     conv_index.push_back(ci++);
+    if (!has_weights) {
+      f = l.fo;
+      continue;
+    }
     const int64_t nk = l.fo * f * l.ext.vol();
     DevBuf kb(c, nk * 4), bb(c, l.fo * 4);
     const auto kind = device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -67,13 +72,24 @@ Model::Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr) : c(
   VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
-ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos) const {
+ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos, const int* pool_modes) const {
   ForwardPlan p;
   p.S = S;
   require(S > 0, "execute: batch must be positive");
   std::vector<int> modes;
-  for (const auto& l : net.layers)
-    if (l.kind == 1) modes.push_back(l.forced >= 0 ? l.forced : 1);
+  for (const auto& l : net.layers) {
+    if (l.kind != 1) continue;
+    int m = l.forced >= 0 ? l.forced : 1;
+    if (pool_modes) {
+      const int want = pool_modes[modes.size()];
+      require(want == 0 || want == 1, "execute: pool mode must be plain (0) or fragments (1)");
+      // planner.cpp:565-566
+      require(l.forced < 0 || l.forced == want,
+              "propagate_shapes: assignment conflicts with a forced pooling mode");
+      m = want;
+    }
+    modes.push_back(m);
+  }
   int64_t viol = -1;
   p.shapes = propagate_shapes(net, Shape{1, net.fin, e}, modes, &viol);
   require(viol < 0, "execute: plan input does not propagate through the network");
@@ -466,6 +482,7 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows)
 
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
                     std::vector<double>* layer_seconds) {
+  require(has_weights, "execute: planning-only model has no weights");
   EventTimer timer(c->stream, layer_seconds != nullptr);
   DevBuf frags(c, p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1));
   // kernel spectra first, so the group sizes below see their footprint
@@ -578,6 +595,7 @@ std::string tune_key(int64_t f, int64_t fo, V3 k) {
 }  // namespace
 
 void Model::tune(int64_t S, V3 e) {
+  require(has_weights, "tune: planning-only model has no weights");
   const ForwardPlan p0 = plan(S, e, nullptr);
   std::map<std::string, LayerCosts> replay;
   double replay_pool = -1;

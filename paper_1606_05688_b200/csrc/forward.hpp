@@ -52,8 +52,13 @@ struct Model {
   std::map<int, LayerCosts> measured;             // conv ordinal -> measured costs
   double pool_elem = -1;                          // measured MPF seconds per input element
 
+  bool has_weights = true;  // false: a planning-only model (plan / plan_bytes)
+
+  // weights == nullptr: planning-only model (no device weights)
   Model(Ctx* ctx, const Net& n, const float* weights, bool device_ptr);
-  ForwardPlan plan(int64_t S, V3 e, const int* conv_algos) const;
+  // pool_modes: one per pool layer (0 plain, 1 fragments) or nullptr (the
+  // network's forced modes, fragments where the network leaves the choice)
+  ForwardPlan plan(int64_t S, V3 e, const int* conv_algos, const int* pool_modes = nullptr) const;
   // bytes the forward needs (inputs + output included) when every FFT layer
   // gets contractions of at least target_rows rows (0: groups of one entry)
   int64_t plan_bytes(const ForwardPlan& p, bool cache_spectra, int64_t target_rows = 0) const;

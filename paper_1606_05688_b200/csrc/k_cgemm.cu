@@ -129,11 +129,10 @@ __global__ void __launch_bounds__(GemmCfg<MT, IT, MB, IB, JC>::THREADS)
 template <int MT, int IT, int MB, int IB, int JC>
 void gemm_t(Ctx* c, GemmArgs a, int64_t nwb) {
   using G = GemmCfg<MT, IT, MB, IB, JC>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_kernel<MT, IT, MB, IB, JC>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    configured = true;
   }
   a.mblocks = int((a.M + MB - 1) / MB);
   a.iblocks = (a.fo + IB - 1) / IB;

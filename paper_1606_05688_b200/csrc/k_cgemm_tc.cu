@@ -388,11 +388,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) cgemm_tc_kernel(GemmArgs a) {
 template <int FO>
 void tc_t(Ctx* c, GemmArgs a) {
   using C = TcCfg<FO>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_tc_kernel<FO>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    configured = true;
   }
   a.mblocks = int((a.M + TC_M - 1) / TC_M);
   const int64_t ntiles = int64_t(a.mblocks) * a.npairs;  // npairs = 8 per 16-frequency line

@@ -150,11 +150,10 @@ void run_direct(Ctx* c, const float* in, const float* w, const float* bias, floa
   const size_t smem = sizeof(float) * (size_t(kvol) * JB +
                                        size_t(TX + g.kx - 1) * (TY + g.ky - 1) * (TZ + kz - 1));
   require(smem <= 200 * 1024, "conv_direct: kernel too large for the direct device kernel");
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(conv_direct_kernel<KZ>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
   }
   dim3 grid(unsigned(g.tiles_x) * g.tiles_y * g.tiles_z, unsigned((g.fo + JB - 1) / JB),
             unsigned(g.S));

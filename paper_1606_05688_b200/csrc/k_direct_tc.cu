@@ -39,7 +39,8 @@ using namespace tc;
 
 constexpr int DT_THREADS = 512;  // 16 warps: two epilogue warpgroups
 constexpr int DT_NS = 8;     // staging slots
-constexpr int DT_RS = 136;   // staged row stride (floats): 128 + kz - 1 <= 136
+constexpr int DT_RS = 140;   // staged row stride (floats): the 16-byte superset of
+                             // 128 + kz - 1 floats (up to 3 more) fits for kz <= 10
 constexpr int DT_ROWS = 16;  // kx * ky <= 16
 
 struct DtGeom {
@@ -366,11 +367,10 @@ __global__ void __launch_bounds__(DT_THREADS, 1) direct_tc_kernel(DtGeom g) {
 template <int N, int K>
 void run_dt(Ctx* c, const DtGeom& g) {
   using C = DtCfg<N, K>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(direct_tc_kernel<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         C::SMEM_LAUNCH));
-    configured = true;
   }
   const unsigned grid = unsigned(std::min<int64_t>(g.tiles, c->num_sms));
   static const bool prof = std::getenv("VXG_DT_PROF") != nullptr;
@@ -436,7 +436,7 @@ int64_t direct_tc_min_maps() {
 bool direct_tc_supported(int64_t f, int64_t fo, V3 k, const void* in) {
   return direct_tc_enabled() && f == 1 && fo % 16 == 0 && fo >= direct_tc_min_maps() && fo <= 80 &&
          k.x * k.y <= DT_ROWS &&
-         k.vol() <= 64 && TC_M + k.z - 1 <= DT_RS &&
+         k.vol() <= 64 && TC_M + k.z - 1 + 3 <= DT_RS &&  // + 3: 16-byte superset of the row
          (reinterpret_cast<uintptr_t>(in) & 15) == 0;  // bulk copies of 16-byte-aligned row supersets
 }
 

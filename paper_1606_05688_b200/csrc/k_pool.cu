@@ -496,6 +496,8 @@ void launch_nan_check(Ctx* c, const float* x, i64 count) {
   check_launch("nan_check_kernel");
 }
 
+void clear_flag_async(Ctx* c) { VXG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream)); }
+
 bool read_and_clear_flag(Ctx* c) {
   int h = 0;
   VXG_CUDA_CHECK(cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

@@ -741,19 +741,17 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
 template <int T>
 void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_kernel<T>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    configured = true;
   }
   if (a.pair && T >= 24) {
     using P = PairCfg<T>;
-    static bool pconf = false;
-    if (!pconf) {
+    static PerDeviceOnce pconf;
+    if (pconf.first()) {
       VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_pair_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
-      pconf = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(2 * nblocks));
@@ -780,19 +778,17 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
 template <int T>
 void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  if (configured.first()) {
     VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_kernel<T>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    configured = true;
   }
   if (a.pair && T >= 24) {
     using P = PairCfg<T>;
-    static bool pconf = false;
-    if (!pconf) {
+    static PerDeviceOnce pconf;
+    if (pconf.first()) {
       VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_pair_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM_INV));
-      pconf = true;
     }
     CUtensorMap ymap{};
     if (a.lw == 2) {

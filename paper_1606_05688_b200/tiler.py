@@ -52,10 +52,11 @@ def plan_tiles(volume: Sequence[int], fov: Sequence[int], tile_out: Sequence[int
         raise ValueError("tiler: volume smaller than the field of view")
     ext = []
     for a in range(3):
+        # a tile's crop is admissible only if its output extent is a multiple of
+        # the MPF stride product; a dense extent that is not gets a shifted last tile
         t = min(int(tile_out[a]), dense[a])
-        if t % align[a] and t != dense[a]:
-            t -= t % align[a]
-        if t <= 0 or (t % align[a] and dense[a] % align[a]):
+        t -= t % align[a]
+        if t <= 0:
             raise ValueError("tiler: tile extent incompatible with the MPF stride")
         ext.append(t)
     axes = [_axis_tiles(dense[a], ext[a]) for a in range(3)]

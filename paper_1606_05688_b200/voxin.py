@@ -209,6 +209,34 @@ def _ptr_of(t):
     return t.ctypes.data_as(C.c_void_p)
 
 
+def _check_out(out, shape, like):
+    """A caller-supplied output must match what the call writes: shape, float32,
+    contiguous, and on the same side (host / device) as the input -- the C-ABI
+    takes raw pointers and cannot check any of this itself."""
+    shape = tuple(int(s) for s in shape)
+    if _is_torch_cuda(like) != _is_torch_cuda(out):
+        raise ValueError("out must live on the same side (host or device) as the input")
+    if _is_torch_cuda(out):
+        import torch
+        if out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != shape \
+                or out.device != like.device:
+            raise ValueError(f"out must be a contiguous float32 CUDA tensor of shape {shape} "
+                             "on the input's device")
+    else:
+        if not isinstance(out, np.ndarray) or out.dtype != np.float32 or not out.flags.c_contiguous \
+                or tuple(out.shape) != shape or not out.flags.writeable:
+            raise ValueError(f"out must be a writeable C-contiguous float32 array of shape {shape}")
+    return out
+
+
+def _check_weights(net, weights):
+    """NetworkWeights check (execute.hpp: one kernel set + bias per conv layer):
+    the flat weight vector must hold exactly net.weight_count() scalars."""
+    n = int(np.prod(weights.shape)) if hasattr(weights, "shape") else len(weights)
+    if n != net.weight_count():
+        raise ValueError(f"weights: {n} scalars given, the network needs {net.weight_count()}")
+
+
 def _same_mem(*args):
     mems = {a.mem for a in args}
     if len(mems) != 1:
@@ -570,6 +598,7 @@ class Model:
     def __init__(self, net: NetworkSpec, weights, ctx: Optional[Context] = None):
         self.ctx = ctx or default_context()
         self.net = net
+        _check_weights(net, weights)
         wi = _Arg(weights)
         p = C.c_void_p()
         check(lib().vxg_model_create(self.ctx.handle, net.handle, wi.ptr, wi.mem, C.byref(p)))
@@ -638,9 +667,13 @@ class Model:
         e = [int(v) for v in input.shape[2:]]
         if int(input.shape[1]) != self.net.features_in:
             raise ValueError("execute: input does not match the network")
+        if len(input.shape) != 5:
+            raise ValueError("execute: input must be 5D (s, f, x, y, z)")
         xi = _Arg(input)
         if out is None:
             out = _out_like(input, self.output_shape(S, e))
+        else:
+            _check_out(out, self.output_shape(S, e), input)
         rep = L.Report()
         check(lib().vxg_model_forward(self._p, xi.mem, xi.ptr, S, i64s(e), _algos(self.net, conv_algos),
                                       1 if cache_spectra else 0, _ptr_of(out), C.byref(rep)))
@@ -661,6 +694,9 @@ class Model:
 def execute(net: NetworkSpec, weights, input, ctx: Optional[Context] = None, conv_algos=None):
     """execute_plan (execute.hpp:388-402) with an all-fragment plan: (dense, report)."""
     ctx = ctx or default_context()
+    if len(input.shape) != 5 or int(input.shape[1]) != net.features_in:
+        raise ValueError("execute: input does not match the network")
+    _check_weights(net, weights)
     S = int(input.shape[0])
     e = [int(v) for v in input.shape[2:]]
     wi, xi = _Arg(weights), _Arg(input)

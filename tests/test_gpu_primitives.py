@@ -177,6 +177,11 @@ def test_conv_random_vs_oracle(oracle, ctx, case):
     (2, (24, 21, 131), 64, (4, 4, 4)),
     (1, (9, 10, 257), 80, (4, 3, 2)),
     (1, (9, 10, 40), 32, (4, 4, 4)),   # 32 maps: FFMA kernel
+    # kz = 7 / 8 with nz % 4 != 0: the 16-byte superset of a staged row is up
+    # to 3 floats longer than 128 + kz - 1 (row overflow)
+    (1, (9, 10, 257), 48, (3, 3, 7)),
+    (1, (8, 9, 259), 64, (2, 2, 8)),
+    (1, (7, 8, 261), 80, (1, 2, 9)),
 ])
 def test_conv_direct_single_input_map_tensor_cores(oracle, ctx, case):
     """f = 1 direct convolution (the first layer of every bundled net) on the

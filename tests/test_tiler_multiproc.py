@@ -38,6 +38,22 @@ def test_plan_tiles_cover_output_exactly_once():
     assert sorted(t.index for m in mine for t in m) == list(range(len(tiles)))
 
 
+def test_plan_tiles_tile_larger_than_unaligned_dense():
+    """tile_out >= dense with dense % align != 0: the tile shrinks to
+    the largest aligned extent and a shifted last tile covers the rest."""
+    vol, fov = (30, 29, 28), (7, 7, 7)  # dense 24, 23, 22
+    tiles = tiler.plan_tiles(vol, fov, (64, 64, 64), (4, 4, 4))
+    dense = [vol[a] - fov[a] + 1 for a in range(3)]
+    cover = np.zeros(dense, np.int32)
+    for t in tiles:
+        assert all(e % 4 == 0 for e in t.out_extent)
+        assert all(t.in_origin[a] + t.in_extent[a] <= vol[a] for a in range(3))
+        sl = tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a]) for a in range(3))
+        cover[sl] += 1
+    assert (cover == 1).all()
+    assert [t.out_extent for t in tiles][0] == (24, 20, 20)
+
+
 def test_run_tiles_batched_streaming_path():
     """The forward_many path (batches of equal-extent tiles) writes exactly what
     the one-tile path writes, and still honours resume."""
