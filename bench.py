@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--quick", action="store_true", help="small extent (profiling / smoke)")
     ap.add_argument("--no-tune", action="store_true", help="modelled (not measured) layer planning")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU test of the N > 1 launch path
     return ap.parse_args()
 
 
@@ -149,6 +150,37 @@ def pick_extent(model, budget_bytes, fov, hi=2048, algos=None, fout=3):
     return best
 
 
+def choose_patch(model, net, fov, budget_bytes, tuned, extent=0, quick=False):
+    """(extent, conv algos) of the bench step: the largest admissible patch whose
+    plan fits the budget, or -- with measured layer costs -- the (patch,
+    first-layer algorithm) pair of highest estimated throughput among the
+    largest few fitting patches: a direct first layer fuses with the MPF after
+    it (its full-resolution output never exists) and so admits a larger patch
+    than an FFT one.  Also used by the GPU parity tests to run the bench's plan."""
+    if extent:
+        return extent, None
+    if quick:
+        return 258, None
+    nconv = sum(1 for l in net.layers if l[0] == "conv")
+    step = 1  # admissible extents repeat with the MPF stride product
+    for l in net.layers:
+        if l[0] == "pool":
+            step *= l[1][0]
+    if not tuned:
+        return pick_extent(model, budget_bytes, fov, fout=net.features_out), None
+    best = None
+    for algos in (None, ["direct"] + ["auto"] * (nconv - 1)):
+        emax = pick_extent(model, budget_bytes, fov, algos=algos, fout=net.features_out)
+        if emax is None:
+            continue
+        for e in range(emax, max(fov, emax - step * 12) - 1, -step):
+            est = sum(l["seconds"] for l in model.plan_info(1, e, algos))
+            score = (e - fov + 1) ** 3 / est if est > 0 else 0
+            if best is None or score > best[0]:
+                best = (score, e, algos)
+    return (best[1], best[2]) if best else (None, None)
+
+
 def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm):
     """sum over layers of max(F_l / P_fp32, B_l / P_hbm) with
     F_fft = 7.5 S (f+f') N^3 log2 N + 2.5 f f' N log2 N (k^2 + kN + N^2) + 8 S f f' #w,
@@ -181,62 +213,163 @@ def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm):
     return total
 
 
+def bundled_nets():
+    """NETS / FOV of paper_1606_05688_b200/bundled_nets.py, loaded by file path:
+    importing the package would map libvxg.so into the process, and the
+    reference arm must run without any of the product's native code."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_vxg_bundled_nets", ROOT / "paper_1606_05688_b200" / "bundled_nets.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.NETS, mod.FOV
+
+
+def reference_steps(ref, net_text, e, plan, warmup, steps, nlayers):
+    """The reference's execute_plan (host-only plan: run_prefix + recombine,
+    proj/include/voxin/execute.hpp:147-226, 388-402) run one layer per step
+    (oracle/ref_shim.cpp ref_stepper_*; bit-identical to execute_plan,
+    tests/test_oracle.py).  A step is one layer of a forward, forwards follow
+    each other from the same input; `warmup` untimed steps, then `steps` timed
+    ones, extended until every layer was timed at least once.  Forward time =
+    sum over layers of the layer's mean timed seconds."""
+    st = ref.stepper(net_text, e, 1, bench_seed(1, e), plan=plan, conv_kind=3, nlayers=nlayers)
+    for _ in range(warmup):
+        st.step()
+    per_layer = {}
+    timed = []
+    while len(timed) < steps or len(per_layer) < nlayers:
+        li, sec, _ = st.step()
+        per_layer.setdefault(li, []).append(sec)
+        timed.append(sec)
+    fwd = sum(sum(v) / len(v) for v in per_layer.values())
+    kinds = st.kinds
+    st.close()
+    return {"forward_seconds": fwd, "timed_steps": len(timed), "step_seconds": timed,
+            "layer_seconds": {int(k): sum(v) / len(v) for k, v in sorted(per_layer.items())}, "kinds": kinds}
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    compiled from the unmodified sources) on all host cores."""
+    compiled from the unmodified sources) on all host cores, through its
+    execute_plan (layer-stepped) with conv forced to fft_task_parallel (the
+    fastest measured reference primitive), every pool MPF; then
+    one forward with the reference planner's own plan (optimize_plan) for
+    context.  No product code is imported."""
     if ws > 1 and rank != 0:
         return
     from oracle.refbind import Ref
-    from paper_1606_05688_b200.bundled_nets import FOV, NETS
+    NETS, FOV = bundled_nets()
     ref = Ref(workers=0)
-    e = SMALLEST[args.net]  # smallest admissible patch: what the CPU path finishes in bounded time
-    # one forward is ~60 s on 16 host cores: at most 1 warm-up + 3 timed forwards
-    # keep the arm within a few minutes (the counts actually run are reported)
-    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))
-    times = []
-    for i in range(warm + steps):
-        secs, spent, vox = ref.net_sample(NETS[args.net], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
-        if i >= warm:
-            times.append(secs)
-    t = sum(times)
+    e = SMALLEST[args.net]  # smallest admissible patch: a forward the CPU path finishes in bounded time
+    text = NETS[args.net]
+    nlayers = sum(1 for l in text.splitlines() if l.startswith(("conv", "pool")))
     vox = (e - FOV[args.net] + 1) ** 3
-    value = vox * len(times) / t
+    main_run = reference_steps(ref, text, e, "forced", args.warmup, args.steps, nlayers)
+    value = vox / main_run["forward_seconds"]
+    planner_run = reference_steps(ref, text, e, "planner", 0, nlayers, nlayers)
+    steps_s = main_run["step_seconds"]
     line = {
         "impl": "reference", "metric": f"output voxels/sec, {args.net} 3D ConvNet sliding-window inference",
-        "value": value, "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
+        "value": value, "unit": "voxels/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(steps_s) / len(steps_s), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.net} full forward, input {e}^3 -> dense {e - FOV[args.net] + 1}^3, "
-                               "all pools MPF, reference host primitives (direct for f=1 layers, "
-                               "fft_task_parallel otherwise)", "net": args.net, "extent": e},
+                               "all pools MPF, conv fft_task_parallel (reference execute_plan, host-only plan)",
+                   "net": args.net, "extent": e,
+                   "step": "one layer of execute_plan's host-only path (the forward runs layer by layer "
+                           "across steps; forward time = sum of mean layer times)",
+                   "timed_steps_run": main_run["timed_steps"]},
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
-                         "sample": f"full {args.net} forward at the smallest admissible patch {e}^3 per step"},
+                         "sample": f"{args.net} at {e}^3: {main_run['timed_steps']} timed layer steps of "
+                                   "the reference execute_plan (fft_task_parallel, MPF), after "
+                                   f"{args.warmup} warm-up steps"},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "forward_seconds": main_run["forward_seconds"],
+        "layer_seconds": main_run["layer_seconds"],
+        "reference_planner_plan": {"kinds": planner_run["kinds"],
+                                   "forward_seconds": planner_run["forward_seconds"],
+                                   "value": vox / planner_run["forward_seconds"],
+                                   "note": "the reference's optimize_plan (HostModel, workers = cores) at "
+                                           f"extent {e}, one forward"},
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args):
-    """Reference CPU path on the box's host cores (rank 0, N = 1): one full n537
-    forward at its smallest admissible patch through oracle/_ref."""
+    """Reference CPU path on the box's host cores (rank 0, N = 1): one full
+    forward (one step per layer) of the reference's execute_plan at the
+    smallest admissible patch through oracle/_ref (no product code)."""
     try:
         from oracle.refbind import Ref
-        from paper_1606_05688_b200.bundled_nets import FOV, NETS
+        NETS, FOV = bundled_nets()
+        ref = Ref(workers=0)
     except Exception as ex:  # pragma: no cover
         return {"value": None, "unit": "voxels/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {ex}"}
-    try:
-        ref = Ref(workers=0)
-    except FileNotFoundError as ex:
-        return {"value": None, "unit": "voxels/s", "cores": 0, "kind": "reference",
-                "sample": f"unavailable: {ex}"}
     e = SMALLEST[args.net]
-    secs, spent, vox = ref.net_sample(NETS[args.net], e, 1, bench_seed(1, e), conv_kind=-1, keep=0)
-    return {"value": vox / secs, "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
-            "seconds": secs,
+    text = NETS[args.net]
+    nlayers = sum(1 for l in text.splitlines() if l.startswith(("conv", "pool")))
+    run = reference_steps(ref, text, e, "forced", 0, nlayers, nlayers)
+    vox = (e - FOV[args.net] + 1) ** 3
+    return {"value": vox / run["forward_seconds"], "unit": "voxels/s", "cores": ref.workers, "kind": "reference",
+            "seconds": run["forward_seconds"],
             "sample": f"one full {args.net} forward at its smallest admissible patch {e}^3 -> dense "
-                      f"{e - FOV[args.net] + 1}^3 (oracle/_ref built from the unmodified reference; "
-                      "direct conv for f=1 layers, fft_task_parallel otherwise; fp32)"}
+                      f"{e - FOV[args.net] + 1}^3: the reference's execute_plan (oracle/_ref, unmodified "
+                      "sources), conv fft_task_parallel, pools MPF, recombined; fp32"}
+
+
+def self_launch(args):
+    """`--gpus N` (N > 1) without a torch.distributed environment: re-run this
+    script under torch.distributed.run with N ranks on this node (rendezvous on
+    127.0.0.1), so a bare `python bench.py --gpus 8` measures 8 GPUs."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_stub(args, ws, rank):
+    """--stub (CPU tests of the N > 1 launch path): the bench's distributed
+    skeleton -- self-launch, barrier, max-over-ranks timing, whole-job value --
+    over gloo with a numpy stand-in step (a translation-equivariant box filter
+    on this rank's own tile); no GPU, no product code."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("gloo")
+    e, fov = 48, 9
+    x = np.random.default_rng(rank).standard_normal((e, e, e)).astype(np.float32)
+
+    def step():
+        c = x.cumsum(0).cumsum(1).cumsum(2)
+        return float(c[-1, -1, -1])
+
+    for _ in range(args.warmup):
+        step()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    elapsed = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    voxels = (e - fov + 1) ** 3
+    if rank == 0:
+        print(json.dumps({"metric": "stub", "value": ws * args.steps * voxels / elapsed, "unit": "voxels/s",
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1e3 * elapsed / args.steps, "scaling": "weak", "stub": True,
+                          "voxels_per_rank_step": voxels, "elapsed_max_over_ranks": elapsed}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -245,6 +378,13 @@ def main():
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.stub:
+        run_stub(args, ws, rank)
+        return
+    if ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
 
     import numpy as np
     import torch
@@ -265,35 +405,9 @@ def main():
     ctx = v.Context(local, budget)
     model = v.Model(net, weights, ctx)
     budget_bytes = ctx.memory()["budget"]
-    nconv = sum(1 for l in net.layers if l[0] == "conv")
-    step = 1  # admissible extents repeat with the MPF stride product
-    for l in net.layers:
-        if l[0] == "pool":
-            step *= l[1][0]
 
     def choose(tuned):
-        """(extent, conv algos): the largest fitting patch, or -- with measured
-        layer costs -- the (patch, first-layer algorithm) pair of highest
-        estimated throughput among the largest few fitting patches: a direct
-        first layer fuses with the MPF after it (its full-resolution output
-        never exists) and so admits a larger patch than an FFT one."""
-        if args.extent:
-            return args.extent, None
-        if args.quick:
-            return 258, None
-        if not tuned:
-            return pick_extent(model, budget_bytes * 0.97, fov, fout=net.features_out), None
-        best = None
-        for algos in (None, ["direct"] + ["auto"] * (nconv - 1)):
-            emax = pick_extent(model, budget_bytes * 0.97, fov, algos=algos, fout=net.features_out)
-            if emax is None:
-                continue
-            for e in range(emax, max(fov, emax - step * 12) - 1, -step):
-                est = sum(l["seconds"] for l in model.plan_info(1, e, algos))
-                score = (e - fov + 1) ** 3 / est if est > 0 else 0
-                if best is None or score > best[0]:
-                    best = (score, e, algos)
-        return (best[1], best[2]) if best else (None, None)
+        return choose_patch(model, net, fov, budget_bytes, tuned, args.extent, args.quick)
 
     e, algos = choose(False)
     if e is None:

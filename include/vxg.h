@@ -72,7 +72,7 @@ const char* vxg_version(void);
 /* ---- context: one per GPU, one host thread per context ------------------- */
 /* The context owns a CUDA stream, a stream-ordered allocator and the HBM budget
  * tracker (the device MemoryTracker of execute.hpp:259-267).  budget <= 0:
- * 90% of the free HBM at creation. */
+ * the free HBM at creation minus a 2.5 GiB reserve. */
 int vxg_ctx_create(int device, int64_t hbm_budget_bytes, vxg_ctx** out);
 int vxg_ctx_destroy(vxg_ctx* ctx);
 int vxg_ctx_sync(vxg_ctx* ctx);

@@ -18,7 +18,13 @@
 //   ref_fill_random     -> cli.cpp:78-84 (restated: cli.cpp is not built)
 //   ref_net_forward     -> execute.hpp:388-402 (host-only plan, theta = L)
 //   ref_net_sample      -> the reference primitives timed layer by layer on a
-//                          fragment-sampled chain (bench cpu_baseline)
+//                          fragment-sampled chain (kept for experiments)
+//   ref_stepper_*       -> execute_plan's host-only path (run_prefix +
+//                          recombine, execute.hpp:147-164, 219-226, 388-402)
+//                          executed one layer per call, with the plan of the
+//                          reference's own optimize_plan (planner.cpp:648-686)
+//                          or a forced conv kind: bench.py's reference arm and
+//                          cpu_baseline (a bench step = one layer of a forward)
 
 #include <chrono>
 #include <cstdint>
@@ -451,6 +457,148 @@ int ref_optimize_plan(const char* net_text, int64_t min_extent, int64_t max_exte
     for (size_t i = 0; i < po.plan->layers.size(); ++i)
       kinds[i] = static_cast<int>(po.plan->layers[i].kind);
   });
+}
+
+
+}  // extern "C"
+
+namespace {
+
+// One forward of execute_plan's host-only path (theta = L), a layer per step.
+struct Stepper {
+  NetworkSpec net;
+  NetworkWeights<float> w;
+  ExecutionPlan plan;
+  Tensor5<float> input, cur;
+  std::vector<i64> conv_at;
+  std::vector<vec3> windows;  // fragment windows in network order
+  size_t li = 0;
+  bool need_input = false;  // a forward completed: the next step starts from the input
+};
+
+LayerContext<float> host_ctx() {
+  // PlanRunner::host_ctx (execute.hpp:247-255) with ExecutionEnv defaults
+  LayerContext<float> ctx;
+  ctx.workers = g_workers;
+  ctx.workspace = FftWorkspace{i64(1) << 50, 64};
+  ctx.profile = RadixProfile::host_default();
+  return ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+// plan_mode 0: the reference planner's own plan (optimize_plan on a HostModel
+// with workers = the worker count, bounds [e, e]); 1: every conv = conv_kind,
+// every pool MPF.  kinds (optional, one per layer) receives the plan's
+// PrimitiveKind values.
+int ref_stepper_create(const char* net_text, int64_t e, uint64_t wseed, uint64_t iseed, int plan_mode,
+                       int conv_kind, void** handle, int* kinds) {
+  return guard([&] {
+    auto* st = new Stepper();
+    try {
+      st->net = parse_network_spec(net_text);
+      st->w = random_weights<float>(st->net, wseed);
+      const Shape5 in{1, st->net.features_in, vec3::cube(e)};
+      if (plan_mode == 0) {
+        HostModel host;
+        host.env.workers = double(g_workers);
+        SearchBounds b;
+        b.min_extent = e;
+        b.max_extent = e;
+        const PlanOutcome po = optimize_plan(st->net, host, b);
+        require(po.feasible(), "ref_stepper: the reference planner found no plan");
+        st->plan = *po.plan;
+        require(st->plan.theta == i64(st->net.layers.size()), "ref_stepper: host-only plan expected");
+      } else {
+        st->plan = host_plan(st->net, in, conv_kind, 1);
+      }
+      st->input = Tensor5<float>(st->plan.input);
+      std::mt19937_64 rng(iseed);
+      std::uniform_real_distribution<double> d(-1.0, 1.0);
+      for (i64 i = 0; i < st->input.size(); ++i) st->input.data()[i] = static_cast<float>(d(rng));
+      i64 c = 0;
+      for (size_t i = 0; i < st->net.layers.size(); ++i) {
+        st->conv_at.push_back(std::holds_alternative<ConvSpec>(st->net.layers[i]) ? c++ : -1);
+        if (const auto* p = std::get_if<PoolSpec>(&st->net.layers[i]))
+          if (st->plan.layers[i].kind == PrimitiveKind::pool_fragments) st->windows.push_back(p->window);
+        if (kinds) kinds[i] = static_cast<int>(st->plan.layers[i].kind);
+      }
+      st->cur = Tensor5<float>(st->input);
+    } catch (...) {
+      delete st;
+      throw;
+    }
+    *handle = st;
+  });
+}
+
+// Runs the next layer (the last one includes recombine_fragments).  *layer =
+// the layer run, *seconds = its wall time, *done = 1 when it completed a
+// forward (the next step starts a new forward from the same input).
+int ref_stepper_step(void* handle, int64_t* layer, double* seconds, int* done) {
+  return guard([&] {
+    auto* st = static_cast<Stepper*>(handle);
+    if (st->need_input) {  // outside the timed step, as measure_throughput copies its input
+      st->cur = Tensor5<float>(st->input);
+      st->need_input = false;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t li = st->li;
+    const LayerPlan& lp = st->plan.layers[li];
+    LayerContext<float> ctx = host_ctx();
+    if (std::holds_alternative<ConvSpec>(st->net.layers[li])) {
+      const ConvLayerParams<float>& p = st->w.convs[size_t(st->conv_at[li])];
+      switch (lp.kind) {  // PlanRunner::host_conv (execute.hpp:281-297)
+        case PrimitiveKind::direct_naive:
+          st->cur = conv_direct(std::move(st->cur), p, ctx, DirectVariant::naive).output;
+          break;
+        case PrimitiveKind::direct_temp:
+          st->cur = conv_direct(std::move(st->cur), p, ctx, DirectVariant::temp_buffer).output;
+          break;
+        case PrimitiveKind::fft_data_parallel:
+          st->cur = conv_fft_data_parallel(std::move(st->cur), p, ctx).output;
+          break;
+        case PrimitiveKind::fft_task_parallel:
+          st->cur = conv_fft_task_parallel(std::move(st->cur), p, ctx).output;
+          break;
+        case PrimitiveKind::fft_staged:
+          st->cur = conv_fft_staged(std::move(st->cur), p, ctx).output;
+          break;
+        default: throw std::invalid_argument("ref_stepper: not a host convolution primitive");
+      }
+    } else {  // PlanRunner::pool (execute.hpp:312-317)
+      const vec3 win = std::get<PoolSpec>(st->net.layers[li]).window;
+      st->cur = lp.kind == PrimitiveKind::pool_fragments ? mpf_pool(std::move(st->cur), win, ctx).output
+                                                         : max_pool(std::move(st->cur), win, ctx).output;
+    }
+    const bool last = li + 1 == st->net.layers.size();
+    if (last && !st->windows.empty())  // PlanRunner::recombine (execute.hpp:219-226)
+      st->cur = recombine_fragments(st->cur, st->windows, st->plan.input.s);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *layer = int64_t(li);
+    *done = last ? 1 : 0;
+    st->li = last ? 0 : li + 1;
+    st->need_input = last;
+  });
+}
+
+// the dense output of the last completed forward (valid until the next step)
+int ref_stepper_output(void* handle, float* out, int64_t* shape5) {
+  return guard([&] {
+    auto* st = static_cast<Stepper*>(handle);
+    const Shape5 s = st->cur.shape();
+    if (shape5) {
+      shape5[0] = s.s; shape5[1] = s.f; shape5[2] = s.n.x; shape5[3] = s.n.y; shape5[4] = s.n.z;
+    }
+    if (out) std::memcpy(out, st->cur.data(), sizeof(float) * size_t(st->cur.size()));
+  });
+}
+
+int ref_stepper_free(void* handle) {
+  delete static_cast<Stepper*>(handle);
+  return 0;
 }
 
 }  // extern "C"

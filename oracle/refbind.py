@@ -70,6 +70,10 @@ class Ref:
             "ref_fill_random": [I, V, L, U],
             "ref_net_forward": [C.c_char_p, I, U, V, L, P, I, I, V, D],
             "ref_net_sample": [C.c_char_p, L, U, U, I, L, D, D, D],
+            "ref_stepper_create": [C.c_char_p, L, U, U, I, I, C.POINTER(C.c_void_p), C.POINTER(C.c_int)],
+            "ref_stepper_step": [V, P, D, C.POINTER(C.c_int)],
+            "ref_stepper_output": [V, V, P],
+            "ref_stepper_free": [V],
         }
         for name, args in sig.items():
             getattr(self.lib, name).argtypes = args
@@ -205,6 +209,48 @@ class Ref:
                                             C.c_uint64(iseed), int(conv_kind), int(keep),
                                             C.byref(ext), C.byref(spent), C.byref(vox)))
         return ext.value, spent.value, vox.value
+
+
+    # PrimitiveKind (proj/include/voxin/cost.hpp:13-24)
+    KINDS = ("direct-naive", "direct-temp", "fft-data-parallel", "fft-task-parallel", "fft-staged",
+             "device-direct-default", "device-direct-precomp", "device-fft", "pool-plain", "pool-fragments")
+
+    def stepper(self, net_text, e, wseed, iseed, plan="forced", conv_kind=3, nlayers=64):
+        """execute_plan's host-only path one layer per step (ref_stepper_*):
+        plan="planner" -> the reference's own optimize_plan at extent e,
+        plan="forced"  -> every conv = conv_kind, every pool MPF."""
+        return RefStepper(self, net_text, e, wseed, iseed, plan, conv_kind, nlayers)
+
+
+class RefStepper:
+    def __init__(self, ref, net_text, e, wseed, iseed, plan, conv_kind, nlayers):
+        self.ref = ref
+        self.h = C.c_void_p()
+        kinds = (C.c_int * nlayers)(*([-1] * nlayers))
+        ref._check(ref.lib.ref_stepper_create(net_text.encode(), int(e), C.c_uint64(wseed), C.c_uint64(iseed),
+                                              0 if plan == "planner" else 1, int(conv_kind), C.byref(self.h), kinds))
+        self.kinds = [Ref.KINDS[k] for k in kinds if k >= 0]
+
+    def step(self):
+        """-> (layer, seconds, done)"""
+        li, sec, done = C.c_int64(), C.c_double(), C.c_int()
+        self.ref._check(self.ref.lib.ref_stepper_step(self.h, C.byref(li), C.byref(sec), C.byref(done)))
+        return li.value, sec.value, bool(done.value)
+
+    def output(self):
+        sh = (C.c_int64 * 5)()
+        self.ref._check(self.ref.lib.ref_stepper_output(self.h, None, sh))
+        out = np.zeros(tuple(sh), np.float32)
+        self.ref._check(self.ref.lib.ref_stepper_output(self.h, _ptr(out), sh))
+        return out
+
+    def close(self):
+        if self.h:
+            self.ref.lib.ref_stepper_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 class Oracle:

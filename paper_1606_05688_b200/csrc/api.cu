@@ -1,6 +1,7 @@
 // The extern "C" boundary (include/vxg.h).  Every entry point converts the
 // internal exceptions into the status codes that mirror the reference's
 // error conventions, and handles host <-> device staging when mem == HOST.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -173,7 +174,9 @@ int vxg_ctx_create(int device, int64_t budget, vxg_ctx** out) {
       VXG_CUDA_CHECK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
       size_t free_b = 0, total_b = 0;
       VXG_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-      c->budget = budget > 0 ? budget : int64_t(double(free_b) * 0.9);
+      // default budget: the HBM free at creation minus a 2.5 GiB reserve (CUDA
+      // context growth, library workspaces, other allocators in the process)
+      c->budget = budget > 0 ? budget : std::max<int64_t>(int64_t(free_b) - (int64_t(5) << 29), int64_t(free_b) / 2);
       VXG_CUDA_CHECK(cudaMalloc(&c->d_flag, sizeof(int)));
       VXG_CUDA_CHECK(cudaMemset(c->d_flag, 0, sizeof(int)));
       init_twiddles();
@@ -315,21 +318,26 @@ int vxg_conv(vxg_ctx* ctx, int algo, int mem, const float* in, int64_t S, int64_
     } else {
       require(algo == VXG_CONV_DIRECT, "vxg_conv: unknown algorithm");
     }
-    double model = 0;
+    // MemoryAudit (memory.hpp:100-103; the band of layers_test.cpp:388-414):
+    // the working set is the call's tensors -- input, kernels, bias, output,
+    // held by the caller (device) or staged here (host) -- plus the workspace.
+    // Model: tensors + kernel spectra + max(raw-spectrum scratch of the
+    // tensor-core split, the X / Y spectrum chunks of the rows used).
+    const double tensors = double(S * f * n.vol() + fo * f * k.vol() + fo + S * fo * no.vol());
+    double model = tensors;
     if (use_fft) {
-      conv_fft_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p, plan, nullptr, 0);
-      // in + out + kernel spectra + the spectrum chunk buffers actually used
-      const int64_t M = S * plan.tiles;
-      model = double(S * f * n.vol() + S * fo * no.vol()) +
-              2.0 * double(plan.nwp) * double(fo * f + M * (f + fo));
+      const int64_t rows = conv_fft_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p, plan, nullptr, 0);
+      const double kspec = double(kernel_spectra_bytes(plan, f, fo)) / 4.0;
+      const double raw = plan.tc ? double(tile_nwp(plan.T, 16) * fo * f * 8) / 4.0 : 0.0;
+      const double chunks = double(fft_chunk_bytes(plan, f, fo, rows)) / 4.0;
+      model += kspec + std::max(raw, chunks);
     } else {
       conv_direct_device(c, xin.p, S, f, n, win.p, fo, k, bin.p, relu != 0, o.p);
-      model = double(S * f * n.vol() + S * fo * no.vol());
     }
     o.finish(c);
     if (audit) {
       VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-      audit->peak = au.peak_scalars();
+      audit->peak = au.peak_scalars() + (mem == VXG_MEM_DEVICE ? tensors : 0.0);
       audit->model = model;
     }
   });
@@ -400,6 +408,7 @@ static int pool_common(vxg_ctx* ctx, int fragments, int mem, const float* in, in
       VXG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
       audit->peak = au.peak_scalars();
       audit->model = double(S * f * n.vol() + S * P * f * no.vol());  // pools row (cost.hpp:347)
+      if (mem == VXG_MEM_DEVICE) audit->peak += audit->model;  // the caller's input and output
     }
   });
 }

@@ -142,10 +142,10 @@ void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, 
   if (tc) tc_wsplit(c, dst, out, tile_nwp(T, 16) / 2, f, fo);
 }
 
-void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
-                     int64_t fo, V3 k, const float* bias, bool relu, float* out,
-                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget, int64_t ipz,
-                     int64_t opz) {
+int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
+                        int64_t fo, V3 k, const float* bias, bool relu, float* out,
+                        const FftPlan& plan, const float2* wspec, int64_t spectra_budget, int64_t ipz,
+                        int64_t opz) {
   const V3 no{n.x - k.x + 1, n.y - k.y + 1, n.z - k.z + 1};
   if (ipz <= 0) ipz = n.z;
   if (opz <= 0) opz = no.z;
@@ -226,6 +226,7 @@ void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const 
     ia.pair = plan.inv_pair;
     launch_tile_inv(c, T, ia, mc * fo);
   }
+  return rows;
 }
 
 void conv_direct_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,

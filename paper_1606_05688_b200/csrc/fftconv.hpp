@@ -108,11 +108,12 @@ int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo);
 // Conv layer drivers on device pointers.  `wspec` (optional) are cached kernel
 // spectra for plan.T; otherwise computed into scratch.  spectra_budget bounds
 // the per-chunk spectrum buffers (bytes; <= 0: what the context budget leaves).
-// ipz / opz: z row pitch of the input / output activations (0: unpadded)
-void conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
-                     int64_t fo, V3 k, const float* bias, bool relu, float* out,
-                     const FftPlan& plan, const float2* wspec, int64_t spectra_budget,
-                     int64_t ipz = 0, int64_t opz = 0);
+// ipz / opz: z row pitch of the input / output activations (0: unpadded).
+// conv_fft_device returns the spectrum chunk rows it used.
+int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
+                        int64_t fo, V3 k, const float* bias, bool relu, float* out,
+                        const FftPlan& plan, const float2* wspec, int64_t spectra_budget,
+                        int64_t ipz = 0, int64_t opz = 0);
 void conv_direct_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
                         int64_t fo, V3 k, const float* bias, bool relu, float* out,
                         int64_t ipz = 0, int64_t opz = 0);

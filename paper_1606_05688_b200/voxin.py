@@ -85,7 +85,7 @@ def _close_all_contexts():
 
 
 class Context:
-    """One per GPU: stream, stream-ordered allocator, HBM budget (bytes; <= 0 = 90% free)."""
+    """One per GPU: stream, stream-ordered allocator, HBM budget (bytes; <= 0: free HBM - 2.5 GiB)."""
 
     def __init__(self, device: int = 0, budget_bytes: int = 0):
         p = C.c_void_p()

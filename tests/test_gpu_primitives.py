@@ -343,3 +343,36 @@ def test_transform_round_trip_large(ctx):
         full_b = np.transpose(sb[0], (2, 1, 0))  # (px, py, zh)
         xh = pad[0] // 2 + 1
         assert rel_error(full_b[:xh, :, :zh], s0[:, :, :zh]) <= 1e-5
+
+
+@pytest.mark.parametrize("mem", ["host", "device"])
+def test_audited_peaks_track_the_memory_models(ctx, mem):
+    """layers_test.cpp:388-414 on the device: every primitive's audited peak
+    (allocator high-water mark of the call + the caller's tensors when they are
+    device-resident) lies in [0.5, 1.15] x its closed-form model, and pools are
+    exact (peak == model).  Shapes: the reference's (4 -> 4, k3, 8^3) plus a
+    tensor-core FFT layer (80 -> 80, k5) and an f = 1 tensor-core direct layer."""
+    import paper_1606_05688_b200 as v
+    rng = np.random.default_rng(50)
+    put = _cuda if mem == "device" else (lambda a: a)
+
+    def band(a):
+        assert a.model > 0
+        assert 0.5 * a.model <= a.peak <= 1.15 * a.model, (a.peak, a.model)
+
+    for (S, f, fo, n, k) in [(1, 4, 4, 8, 3), (2, 80, 80, 40, 5), (1, 1, 80, 60, 4)]:
+        w = (rng.uniform(-1, 1, (fo, f, k, k, k)) * 0.1).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+        x = rng.uniform(-1, 1, (S, f, n, n, n)).astype(np.float32)
+        p = v.ConvLayerParams(put(w), put(b), "relu")
+        band(v.conv_direct(put(x), p, ctx).audit)
+        band(v.conv_fft_data_parallel(put(x), p, ctx).audit)
+        band(v.conv_fft_task_parallel(put(x), p, ctx).audit)
+        band(v.conv_fft_staged(put(x), p, ctx).audit)
+    pin = put(rng.uniform(-1, 1, (2, 3, 9, 9, 9)).astype(np.float32))
+    rp = v.max_pool(pin, (3, 3, 3), ctx).audit
+    band(rp)
+    assert rp.peak == rp.model
+    rf = v.mpf_pool(pin, (2, 2, 2), ctx).audit
+    band(rf)
+    assert rf.peak == rf.model

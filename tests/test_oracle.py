@@ -93,3 +93,26 @@ def test_toy_nets(golden, oracle):
         got = oracle.net_forward(layers, w, x)
         assert got.shape == tuple(m["out_shape"])
         assert rel_error(got, g[f"{name}_out64"]) < 1e-6, name
+
+
+def test_reference_stepper_is_execute_plan():
+    """bench.py's reference arm runs execute_plan's host-only path one layer per
+    step (oracle/ref_shim.cpp ref_stepper_*): a completed stepped forward equals
+    the reference's execute_plan on the same plan bit for bit, forward after
+    forward, and the planner variant takes the reference planner's own kinds."""
+    from oracle.refbind import REF_SO, Ref
+    if not REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    ref = Ref(2)
+    net = "input 1\nconv 4 3 relu\npool 2 mpf\nconv 4 3 relu\npool 2 mpf\nconv 2 3\n"
+    x = ref.fill_random(21 ** 3, 5).reshape(1, 1, 21, 21, 21)
+    st = ref.stepper(net, 21, 1, 5, plan="forced", conv_kind=3)
+    assert st.kinds == ["fft-task-parallel", "pool-fragments"] * 2 + ["fft-task-parallel"]
+    for _ in range(2):
+        steps = [st.step() for _ in range(5)]
+        assert [s[0] for s in steps] == list(range(5)) and steps[-1][2]
+        got = st.output()
+        want, _ = ref.net_forward(net, 1, x, conv_kind=3, prec=32, out_shape=got.shape)
+        assert got.tobytes() == want.tobytes()
+    pl = ref.stepper(net, 21, 1, 5, plan="planner")
+    assert len(pl.kinds) == 5 and pl.kinds[1] in ("pool-fragments", "pool-plain")

@@ -139,3 +139,23 @@ def test_two_rank_gather_gloo():
     assert err < 1e-3
     assert tmax == 2.0
     assert n0 > 0
+
+
+def test_bench_self_launches_n_ranks():
+    """`python bench.py --gpus 2` (no torchrun, no WORLD_SIZE) re-runs itself
+    under torch.distributed.run with 2 ranks; the line reports n_gpus 2 and the
+    whole-job value = ranks x steps x voxels / max-over-ranks time (the --stub
+    step keeps it on CPU / gloo)."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--stub", "--steps", "3",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["steps"] == 3
+    assert d["value"] == pytest.approx(2 * 3 * d["voxels_per_rank_step"] / d["elapsed_max_over_ranks"])
