@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="small extent (profiling / smoke)")
     ap.add_argument("--no-tune", action="store_true", help="modelled (not measured) layer planning")
     ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU test of the N > 1 launch path
+    ap.add_argument("--ref-planner", action="store_true",
+                    help="--impl reference: also time one forward with the reference planner's own plan")
     return ap.parse_args()
 
 
@@ -267,7 +269,9 @@ def run_reference(args, ws, rank):
     vox = (e - FOV[args.net] + 1) ** 3
     main_run = reference_steps(ref, text, e, "forced", args.warmup, args.steps, nlayers)
     value = vox / main_run["forward_seconds"]
-    planner_run = reference_steps(ref, text, e, "planner", 0, nlayers, nlayers)
+    # the reference planner's own plan (fft_data_parallel everywhere for n537:
+    # ~330 s per forward on 16 cores) only on request, to keep the arm to minutes
+    planner_run = reference_steps(ref, text, e, "planner", 0, nlayers, nlayers) if args.ref_planner else None
     steps_s = main_run["step_seconds"]
     line = {
         "impl": "reference", "metric": f"output voxels/sec, {args.net} 3D ConvNet sliding-window inference",
@@ -287,12 +291,12 @@ def run_reference(args, ws, rank):
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "forward_seconds": main_run["forward_seconds"],
         "layer_seconds": main_run["layer_seconds"],
-        "reference_planner_plan": {"kinds": planner_run["kinds"],
-                                   "forward_seconds": planner_run["forward_seconds"],
-                                   "value": vox / planner_run["forward_seconds"],
-                                   "note": "the reference's optimize_plan (HostModel, workers = cores) at "
-                                           f"extent {e}, one forward"},
     }
+    if planner_run:
+        line["reference_planner_plan"] = {
+            "kinds": planner_run["kinds"], "forward_seconds": planner_run["forward_seconds"],
+            "value": vox / planner_run["forward_seconds"],
+            "note": f"the reference's optimize_plan (HostModel, workers = cores) at extent {e}, one forward"}
     print(json.dumps(line), flush=True)
 
 

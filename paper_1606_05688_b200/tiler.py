@@ -7,13 +7,21 @@ output box plus a halo of fov - 1.  Tiles are independent (translation
 equivariance), so ranks process disjoint tile sets with no data-path
 collective; the last tile along an axis shifts inward instead of padding, and
 only the part of it no earlier tile wrote is stored.  Outputs are idempotent
-per tile, which makes resume trivial (``done`` set).  An optional gather
-brings every rank's tiles to rank 0 over torch.distributed (NCCL over
-NVLink on GPUs, gloo on CPU).
+per tile, which makes resume trivial (``done`` set).
+
+Host memory.  The input volume is never copied per rank: any array-like with
+``shape`` and slicing works -- an ``np.memmap`` of a volume file (every rank
+maps the same file; crops page in on demand), an in-memory array, or a
+``SyntheticVolume`` that generates crops on the fly.  Outputs go straight into
+a shared output file (``out_path``: every rank writes its disjoint tiles into
+one ``.npy`` memmap, no gather at all on one node) or, with ``gather=True``,
+to rank 0 over torch.distributed point-to-point (NCCL over NVLink on GPUs,
+gloo on CPU), the sends of all of a rank's tiles in flight at once.
 """
 from __future__ import annotations
 
 import itertools
+import time
 from dataclasses import dataclass
 from typing import Callable, Iterable, Optional, Sequence
 
@@ -74,85 +82,179 @@ def assign(tiles: Sequence[Tile], rank: int, world: int) -> list:
     return [t for t in tiles if t.index % world == rank]
 
 
+class SyntheticVolume:
+    """A (S, f, X, Y, Z) float32 volume defined voxel by voxel by a
+    counter-based generator (splitmix64 of the flat index and the seed ->
+    U(-1, 1) on 24 bits), so any crop is generated on demand, identically on
+    every rank and in any order, without the volume existing in host memory
+    (C5: 2048^3 = 34 GB).  This is the documented deviation SURVEY 8(d) allows
+    from fill_random's sequential mt19937_64 stream.  device="cuda" computes
+    the hash on the GPU (a 634^3 crop in milliseconds instead of seconds of
+    host integer work) and returns the crop as a host array, like a volume
+    file would."""
+
+    def __init__(self, shape, seed: int = 1, device: str = "cpu"):
+        self.shape = tuple(int(s) for s in shape)
+        self.seed = np.uint64(seed)
+        self.dtype = np.dtype(np.float32)
+        self.device = device
+
+    @staticmethod
+    def _mix(z):
+        """splitmix64 finaliser on int64 tensors (wrapping arithmetic; logical
+        right shifts emulated by masking the sign-extended bits)."""
+        def shr(v, k):
+            return (v >> k) & ((1 << (64 - k)) - 1)
+        z = (z ^ shr(z, 30)) * -4658895280553007687   # 0xBF58476D1CE4E5B9
+        z = (z ^ shr(z, 27)) * -7723592293110705685   # 0x94D049BB133111EB
+        return z ^ shr(z, 31)
+
+    def __getitem__(self, key):
+        import torch
+        if not isinstance(key, tuple):
+            key = (key,)
+        key = key + (slice(None),) * (5 - len(key))
+        rng = [range(*k.indices(n)) for k, n in zip(key, self.shape)]
+        if any(r.step != 1 for r in rng):
+            raise ValueError("SyntheticVolume: unit-stride slices only")
+        _, F, X, Y, Z = self.shape
+        idx = [torch.arange(r.start, r.stop, dtype=torch.int64, device=self.device) for r in rng]
+        # flat index, built axis by axis with broadcasting (no 5-D meshgrid)
+        flat = idx[0].view(-1, 1, 1, 1, 1) * F + idx[1].view(1, -1, 1, 1, 1)
+        flat = flat * X + idx[2].view(1, 1, -1, 1, 1)
+        flat = flat * Y + idx[3].view(1, 1, 1, -1, 1)
+        flat = flat * Z + idx[4].view(1, 1, 1, 1, -1)
+        seed_term = (int(self.seed) * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        if seed_term >= 1 << 63:
+            seed_term -= 1 << 64
+        h = self._mix(flat + seed_term)
+        u = ((h >> 40) & 0xFFFFFF).to(torch.float32) * (2.0 / (1 << 24)) - 1.0
+        return u.cpu().numpy()
+
+
+def _crop(volume, t: Tile):
+    sl = tuple(slice(t.in_origin[a], t.in_origin[a] + t.in_extent[a]) for a in range(3))
+    return np.ascontiguousarray(volume[(slice(None), slice(None)) + sl], dtype=np.float32)
+
+
+def _owned(res, t: Tile):
+    rel = tuple(slice(t.write_origin[a] - t.out_origin[a],
+                      t.write_origin[a] - t.out_origin[a] + t.write_extent[a]) for a in range(3))
+    return res[(slice(None), slice(None)) + rel]
+
+
+def _dst(t: Tile):
+    return (slice(None), slice(None)) + tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a])
+                                              for a in range(3))
+
+
 def run_tiles(forward: Callable, volume, tiles: Iterable[Tile], out=None,
-              done: Optional[set] = None, forward_many: Optional[Callable] = None, batch: int = 4):
+              done: Optional[set] = None, forward_many: Optional[Callable] = None, batch: int = 4,
+              timings: Optional[list] = None, keep_blocks: bool = True):
     """forward(crop (1, f, *in_extent)) -> (1, f_out, *out_extent) array.
-    Writes each tile's owned region into `out` (dense, (1, f_out, *dense)) if
-    given; returns {tile index: owned block}.  Tiles in `done` are skipped.
+    Writes each tile's owned region into `out` (dense, (1, f_out, *dense); an
+    array or a shared memmap) if given; returns {tile index: owned block}
+    (empty when keep_blocks is False).  Tiles in `done` are skipped.
     forward_many(list of crops) -> list of results (optional): tiles of one
     extent then run `batch` at a time through it, so uploads and downloads of
-    neighbouring tiles overlap the forwards."""
+    neighbouring tiles overlap the forwards.  `timings` (optional list) gets
+    one {"tiles", "crop_s", "forward_s", "write_s"} record per batch."""
     blocks = {}
     todo = [t for t in tiles if not (done is not None and t.index in done)]
-
-    def crop_of(t):
-        sl = tuple(slice(t.in_origin[a], t.in_origin[a] + t.in_extent[a]) for a in range(3))
-        return np.ascontiguousarray(volume[(slice(None), slice(None)) + sl], dtype=np.float32)
-
-    results = {}
-    if forward_many is not None:
-        for b0 in range(0, len(todo), batch):
-            grp = todo[b0:b0 + batch]
-            same = all(t.in_extent == grp[0].in_extent for t in grp)
-            outs = forward_many([crop_of(t) for t in grp]) if same else [forward(crop_of(t)) for t in grp]
-            for t, r in zip(grp, outs):
-                results[t.index] = r
-    for t in todo:
-        res = np.asarray(results.pop(t.index)) if t.index in results else np.asarray(forward(crop_of(t)))
-        rel = tuple(slice(t.write_origin[a] - t.out_origin[a],
-                          t.write_origin[a] - t.out_origin[a] + t.write_extent[a]) for a in range(3))
-        block = res[(slice(None), slice(None)) + rel]
-        if out is not None:
-            dst = tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a])
-                        for a in range(3))
-            out[(slice(None), slice(None)) + dst] = block
-        blocks[t.index] = block
-        if done is not None:
-            done.add(t.index)
+    step = batch if forward_many is not None else 1
+    for b0 in range(0, len(todo), step):
+        grp = todo[b0:b0 + step]
+        t0 = time.perf_counter()
+        crops = [_crop(volume, t) for t in grp]
+        t1 = time.perf_counter()
+        same = all(t.in_extent == grp[0].in_extent for t in grp)
+        if forward_many is not None and same and len(grp) > 1:
+            results = forward_many(crops)
+        else:
+            results = [forward(c) for c in crops]
+        t2 = time.perf_counter()
+        for t, r in zip(grp, results):
+            block = _owned(np.asarray(r), t)
+            if out is not None:
+                out[_dst(t)] = block
+            if keep_blocks:
+                blocks[t.index] = block
+            if done is not None:
+                done.add(t.index)
+        if timings is not None:
+            timings.append({"tiles": [t.index for t in grp], "crop_s": t1 - t0, "forward_s": t2 - t1,
+                            "write_s": time.perf_counter() - t2})
     return blocks
 
 
 def gather_to_root(blocks: dict, tiles: Sequence[Tile], out, f_out: int, device="cpu"):
-    """Rank r sends its owned blocks to rank 0 (torch.distributed point-to-point;
-    NCCL over NVLink when device is CUDA).  Rank 0 writes them into `out`."""
+    """Every rank's owned blocks to rank 0 (torch.distributed point-to-point;
+    NCCL over NVLink when device is CUDA).  A sender posts all its sends at
+    once (isend) and waits at the end; rank 0 posts one receive per remote
+    tile and writes each block into `out` as it completes, so transfers
+    overlap each other and rank 0's copies."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(), dist.get_world_size()
+    if rank != 0:
+        bufs, reqs = [], []
+        for t in tiles:
+            if t.index % world == rank:
+                b = torch.from_numpy(np.ascontiguousarray(blocks[t.index])).to(device)
+                bufs.append(b)
+                reqs.append(dist.isend(b, dst=0))
+        for r in reqs:
+            r.wait()
+        return
+    pending = []
     for t in tiles:
         owner = t.index % world
-        shape = (1, f_out) + tuple(t.write_extent)
         if owner == 0:
+            out[_dst(t)] = blocks[t.index]
             continue
-        if rank == owner:
-            dist.send(torch.from_numpy(np.ascontiguousarray(blocks[t.index])).to(device), dst=0)
-        elif rank == 0:
-            buf = torch.empty(shape, dtype=torch.float32, device=device)
-            dist.recv(buf, src=owner)
-            dst = tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a])
-                        for a in range(3))
-            out[(slice(None), slice(None)) + dst] = buf.cpu().numpy()
+        buf = torch.empty((1, f_out) + tuple(t.write_extent), dtype=torch.float32, device=device)
+        pending.append((t, buf, dist.irecv(buf, src=owner)))
+    for t, buf, req in pending:
+        req.wait()
+        out[_dst(t)] = buf.cpu().numpy()
+
+
+def open_shared_output(path, shape, rank: int, world: int):
+    """One .npy memmap every rank writes its disjoint tiles into (rank 0
+    creates it; the others open it after a barrier)."""
+    out = None
     if rank == 0:
-        for t in tiles:
-            if t.index % world == 0:
-                dst = tuple(slice(t.write_origin[a], t.write_origin[a] + t.write_extent[a])
-                            for a in range(3))
-                out[(slice(None), slice(None)) + dst] = blocks[t.index]
+        out = np.lib.format.open_memmap(str(path), mode="w+", dtype=np.float32, shape=tuple(shape))
+        out.flush()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank != 0:
+        out = np.load(str(path), mmap_mode="r+")
+    return out
 
 
 def infer_volume(model, volume, tile_out, rank: int = 0, world: int = 1, gather: bool = True,
-                 done: Optional[set] = None):
-    """Dense inference of `volume` (1, f_in, X, Y, Z) with a vxg Model, tiles
-    distributed round-robin over ranks.  Returns the dense output on rank 0
-    (gathered) or this rank's blocks."""
+                 done: Optional[set] = None, out_path=None, batch: int = 4, timings: Optional[list] = None,
+                 tile_subset: Optional[Sequence[int]] = None):
+    """Dense inference of `volume` (1, f_in, X, Y, Z: ndarray, np.memmap or
+    SyntheticVolume) with a vxg Model, tiles distributed round-robin over
+    ranks.  With out_path every rank writes into one shared .npy memmap
+    (returned on every rank); otherwise rank 0 gets the gathered dense output
+    (gather=True) and other ranks their blocks.  tile_subset restricts the run
+    to those tile indices (sampling a big volume)."""
     fov = model.net.field_of_view()
     align = [1, 1, 1]
     for l in model.net.layers:
         if l[0] == "pool":
             align = [align[a] * l[1][a] for a in range(3)]
     tiles = plan_tiles(volume.shape[2:], fov, tile_out, align)
+    if tile_subset is not None:
+        keep = set(int(i) for i in tile_subset)
+        tiles = [t for t in tiles if t.index in keep]
     mine = assign(tiles, rank, world)
     dense = tuple(int(volume.shape[2 + a]) - fov[a] + 1 for a in range(3))
-    out = np.zeros((1, model.net.features_out) + dense, np.float32) if (rank == 0 or world == 1) else None
+    shape = (1, model.net.features_out) + dense
 
     def fwd(crop):
         res, _ = model.forward(np.ascontiguousarray(crop, np.float32))
@@ -162,8 +264,19 @@ def infer_volume(model, volume, tile_out, rank: int = 0, world: int = 1, gather:
         res, _ = model.forward_many(crops)
         return res
 
-    blocks = run_tiles(fwd, volume, mine, out if world == 1 else None, done,
-                       forward_many=fwd_many if hasattr(model, "forward_many") else None)
+    many = fwd_many if hasattr(model, "forward_many") else None
+    if out_path is not None:
+        out = open_shared_output(out_path, shape, rank, world)
+        run_tiles(fwd, volume, mine, out, done, forward_many=many, batch=batch, timings=timings,
+                  keep_blocks=False)
+        out.flush()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        return out
+    out = np.zeros(shape, np.float32) if (rank == 0 or world == 1) else None
+    blocks = run_tiles(fwd, volume, mine, out if world == 1 else None, done, forward_many=many, batch=batch,
+                       timings=timings, keep_blocks=world > 1)
     if world > 1 and gather:
         gather_to_root(blocks, tiles, out, model.net.features_out,
                        device="cuda" if _cuda_dist() else "cpu")

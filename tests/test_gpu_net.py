@@ -276,12 +276,13 @@ def test_bench_patch_full_size_vs_direct_crops(ctx):
 
 def test_network_forward_rejects_nan_input(ctx):
     """mpf_pool's check_no_nan (layers.hpp:111-116, :429) inside the network
-    forward: a NaN voxel reaches the first MPF through the direct first layer ->
+    forward: a NaN voxel reaches the first MPF through an identity first conv ->
     std::invalid_argument / ValueError, for host and device inputs; the flag
-    does not leak into the next (clean) forward."""
+    does not leak into the next (clean) forward.  (After a ReLU conv the NaN is
+    gone, in the reference as here: activate() maps NaN to 0, layers.hpp:105-108.)"""
     import torch
     import paper_1606_05688_b200 as v
-    net = v.parse_network_spec("input 1\nconv 4 3 relu\npool 2 mpf\nconv 4 3 relu\npool 2 mpf\nconv 2 3\n")
+    net = v.parse_network_spec("input 1\nconv 4 3\npool 2 mpf\nconv 4 3 relu\npool 2 mpf\nconv 2 3\n")
     w = v.random_weights(net, 9003)
     model = v.Model(net, w, ctx)
     x = v.fill_random((1, 1, 21, 21, 21), 9103)
@@ -296,3 +297,8 @@ def test_network_forward_rejects_nan_input(ctx):
         assert np.isfinite(out).all()
     with pytest.raises(ValueError, match="NaN"):
         model.forward_many([bad, x])
+    # a network starting with a pool rejects a NaN input directly
+    pnet = v.parse_network_spec("input 1\npool 2 mpf\nconv 2 3\n")
+    pm = v.Model(pnet, v.random_weights(pnet, 1), ctx)
+    with pytest.raises(ValueError, match="NaN"):
+        pm.forward(bad)
