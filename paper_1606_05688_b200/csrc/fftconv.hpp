@@ -77,6 +77,12 @@ void launch_cgemm_tc(Ctx* c, const GemmArgs& a, int64_t npairs);    // tcgen05, 
 // pre-split (tf32 hi/lo, UMMA layout) kernel spectra for the tensor-core path
 int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
 void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
+// quad-frequency tiles (k_cgemm_q.cu, the default tensor-core contraction):
+// sector-complete epilogue stores, pass-split accumulators
+bool tc_quad_enabled();
+int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
+void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
+void launch_cgemm_q(Ctx* c, const GemmArgs& a, int64_t npairs);
 
 // Tile-size choice for a layer: minimises the modelled cost of transforms +
 // contraction over the supported sizes (or honours T_forced > 0).

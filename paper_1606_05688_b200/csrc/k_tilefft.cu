@@ -50,8 +50,6 @@ void init_twiddles() {
   VXG_CUDA_CHECK(cudaMemcpyToSymbol(c_twiddle, h.data(), sizeof(float2) * h.size()));
 }
 
-namespace {
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                            const uint64_t* strides, const uint32_t* box) {
@@ -75,6 +73,8 @@ void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uin
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw cuda_failure("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
+
+namespace {
 
 template <int T>
 struct TileCfg {

@@ -376,3 +376,20 @@ def test_audited_peaks_track_the_memory_models(ctx, mem):
     rf = v.mpf_pool(pin, (2, 2, 2), ctx).audit
     band(rf)
     assert rf.peak == rf.model
+
+
+@pytest.mark.parametrize("fo", [16, 80])
+def test_conv_fft_pair_tile_contraction_kept(oracle, ctx, monkeypatch, fo):
+    """The earlier pair-tile tcgen05 contraction (VXG_TC_PAIR=1: 2 frequencies
+    x all maps per tile, 16-byte epilogue stores) stays selectable for A/B
+    timing; it must agree with the C oracle like the default quad tiles."""
+    import paper_1606_05688_b200 as v
+    monkeypatch.setenv("VXG_TC_PAIR", "1")
+    S, f, k, T = 2, 16, (3, 2, 3), 16
+    n = (T + 5, 2 * T - 3, T + 2)
+    rng = np.random.default_rng(fo + 1)
+    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 18))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=True, ctx=ctx)
+    assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4

@@ -72,6 +72,23 @@ __global__ void pieces(float4* Y) {
   }
 }
 
+// quad layout [w/4][row][map/4][4 maps][4 w]: tile = 128 rows x 1 pair x 80
+// maps, lane = map: a warp instruction writes 32 pieces at 32-byte stride
+// (8 lines, half of each; the CTA of the other pair writes the other half)
+__global__ void p6(float4* Y) {
+  const int ntiles = NWB * 8 * (ROWS / MB);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int pip = t & 7, rest = t >> 3;
+    const int mb = rest % (ROWS / MB), wb = rest / (ROWS / MB);
+    const int pair = wb * 8 + pip, pq = pair >> 1, half = pair & 1;
+    const float4 v = make_float4(float(lane), float(t), 1.f, 2.f);
+    for (int r = w; r < MB; r += 4)
+      for (int i0 = 0; i0 < CH; i0 += 32)
+        if (i0 + lane < CH) Y[((int64_t(pq) * ROWS + mb * MB + r) * CH + i0 + lane) * 2 + half] = v;
+  }
+}
+
 // 16-byte pieces, one CTA writes all 8 pairs of its (line block, row block)
 __global__ void p2(float4* Y) {
   const int ntiles = NWB * (ROWS / MB);
@@ -119,6 +136,7 @@ int main() {
     rep("P1 16B x-CTA lane=row", timeit([&] { pieces<1, false><<<grid, THREADS>>>(Y); }));
     rep("P1m 16B x-CTA lane=map", timeit([&] { pieces<1, true><<<grid, THREADS>>>(Y); }));
     rep("P2 16B same-CTA", timeit([&] { p2<<<grid, THREADS>>>(Y); }));
+    rep("P6 quad lane=map", timeit([&] { p6<<<grid, THREADS>>>(Y); }));
     rep("P3 32B x-CTA", timeit([&] { pieces<2, false><<<grid, THREADS>>>(Y); }));
     rep("P4 64B x-CTA", timeit([&] { pieces<4, false><<<grid, THREADS>>>(Y); }));
     rep("P5 128B lines", timeit([&] { pieces<8, false><<<grid, THREADS>>>(Y); }));
