@@ -524,14 +524,26 @@ def main():
     if ds["flops"] > 0 and dom == "cgemm" and tc_used:
         # tcgen05 kind::tf32 with a 3xTF32 split: 3 tensor MMAs per real product,
         # so the algorithmic-fp32 ceiling is the tf32 peak (1/2 of the measured
-        # dense bf16 peak) / 3
-        ach = ds["flops"] / ds["seconds"] / 1e12
-        tpeak = peaks.get("bf16_tflops", 1695.1) / 2.0 / 3.0
-        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tpeak,
-                "unit": "TFLOP/s", "frac": ach / tpeak,
-                "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peaks_src}) / 2 (tf32) / 3 (3xTF32 split)",
-                "vs_fp32_ffma_peak": ach / ffma_peak,
-                "hbm_frac": ds["bytes"] / ds["seconds"] / 1e9 / peaks["hbm_gbs"]}
+        # dense bf16 peak) / 3.  The contraction also moves X + Y + W through HBM:
+        # report against whichever bound is slower for its per-launch work.
+        tflops = ds["flops"] / ds["seconds"] / 1e12
+        gbps = ds["bytes"] / ds["seconds"] / 1e9
+        # sustained figure: the contraction runs inside a seconds-long step
+        tkey = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
+        tpeak = peaks.get(tkey, 1395.3) / 2.0 / 3.0
+        t_tensor = ds["flops"] / (tpeak * 1e12)
+        t_hbm = ds["bytes"] / (peaks["hbm_gbs"] * 1e9)
+        if t_hbm >= t_tensor:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": gbps, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": gbps / peaks["hbm_gbs"], "peak_source": peaks_src,
+                    "tensor_frac": tflops / tpeak}
+        else:
+            roof = {"kernel": dom, "bound": "tensor", "achieved": tflops, "peak": tpeak,
+                    "unit": "TFLOP/s", "frac": tflops / tpeak,
+                    "peak_source": f"MEASURED_PEAKS.json {tkey} ({peaks_src}) / 2 (tf32) / 3 (3xTF32 split)",
+                    "hbm_frac": gbps / peaks["hbm_gbs"]}
+        roof["tensor_peak_tflops"] = tpeak
+        roof["vs_fp32_ffma_peak"] = tflops / ffma_peak
     elif ds["flops"] > 0:
         ach = ds["flops"] / ds["seconds"] / 1e12
         roof = {"kernel": dom, "bound": "fp32", "achieved": ach, "peak": ffma_peak,

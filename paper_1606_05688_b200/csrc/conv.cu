@@ -76,8 +76,9 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tiles = p.nt.vol();
     p.lw = 16;
     p.tc = tc;
-    p.pair = (T == 32 || T == 24) && tile_pair_enabled();  // measured wins (other T: one CTA is as fast)
-    p.inv_pair = (T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled();  // measured wins
+    // measured wins (other T <= 32: one CTA is as fast); T >= 36 runs on pairs only
+    p.pair = ((T == 32 || T == 24) && tile_pair_enabled()) || T >= 36;
+    p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 36;
     p.ylw = (tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
     p.nwp = tile_nwp(T, p.lw);
     const double M = double(S) * double(p.tiles);

@@ -263,23 +263,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       long long t1 = a.prof ? clock64() : 0;
       cw += t1 - t0;
       const uint8_t* raw = smem + s * Q_RAW + c * a.raw_row;
-      float4 xv[8];
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch) xv[ch] = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
-      mbar_arrive(&rfree[s]);  // the box may be refilled
-      if (a.prof) cb += clock64() - t1;
-      t1 = a.prof ? clock64() : 0;
-      if (g >= C::AS) mbar_wait(&aempty[as], aph ^ 1u);  // the MMAs reading this A slot are done
-      if (a.prof) {
-        const long long t2 = clock64();
-        cw += t2 - t1;
-        t1 = t2;
-      }
-      // A slot columns: ((w*2 + comp)*2 + hi/lo)*8 + channel
+      // split X row c into tf32 hi/lo: A slot columns ((w*2 + comp)*2 + hi/lo)*8 + channel
       uint32_t u[64];
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        const float4 v = xv[ch];
+        const float4 v = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float x = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -288,6 +276,18 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
           u[(e * 2 + 0) * 8 + ch] = __float_as_uint(hi);
           u[(e * 2 + 1) * 8 + ch] = __float_as_uint(lo);
         }
+      }
+      // the box may be refilled: order these generic-proxy reads before the
+      // producer's next TMA (async-proxy) write into the slot
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(&rfree[s]);
+      if (a.prof) cb += clock64() - t1;
+      t1 = a.prof ? clock64() : 0;
+      if (g >= C::AS) mbar_wait(&aempty[as], aph ^ 1u);  // the MMAs reading this A slot are done
+      if (a.prof) {
+        const long long t2 = clock64();
+        cw += t2 - t1;
+        t1 = t2;
       }
       const uint32_t ta = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::ACOL + 64 * as);
       if (!(a.dbg & 8)) asm volatile(

@@ -738,15 +738,16 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
   }
 }
 
+// T whose whole spectrum fits one CTA's shared memory (else: CTA pairs only)
+template <int T>
+constexpr bool single_fits() {
+  return TileCfg<T>::SMEM <= 232448 && TileCfg<T>::THREADS <= 1024;
+}
+
 template <int T>
 void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
-  static PerDeviceOnce configured;
-  if (configured.first()) {
-    VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_kernel<T>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  }
-  if (a.pair && T >= 24) {
+  if ((a.pair && T >= 24) || !single_fits<T>()) {
     using P = PairCfg<T>;
     static PerDeviceOnce pconf;
     if (pconf.first()) {
@@ -770,20 +771,22 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
     check_launch("tile_fwd_pair_kernel");
     return;
   }
-  tile_fwd_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
-  c->counted();
-  check_launch("tile_fwd_kernel");
+  if constexpr (single_fits<T>()) {
+    static PerDeviceOnce configured;
+    if (configured.first()) {
+      VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    }
+    tile_fwd_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
+    c->counted();
+    check_launch("tile_fwd_kernel");
+  }
 }
 
 template <int T>
 void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
-  static PerDeviceOnce configured;
-  if (configured.first()) {
-    VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_kernel<T>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  }
-  if (a.pair && T >= 24) {
+  if ((a.pair && T >= 24) || !single_fits<T>()) {
     using P = PairCfg<T>;
     static PerDeviceOnce pconf;
     if (pconf.first()) {
@@ -815,9 +818,16 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
     check_launch("tile_inv_pair_kernel");
     return;
   }
-  tile_inv_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
-  c->counted();
-  check_launch("tile_inv_kernel");
+  if constexpr (single_fits<T>()) {
+    static PerDeviceOnce configured;
+    if (configured.first()) {
+      VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    }
+    tile_inv_kernel<T><<<unsigned(nblocks), C::THREADS, C::SMEM, c->stream>>>(a);
+    c->counted();
+    check_launch("tile_inv_kernel");
+  }
 }
 
 }  // namespace
@@ -839,7 +849,9 @@ bool inv_pair_enabled() {
 }
 
 // supported tile FFT sizes (even, {2,3,5,7}-smooth)
-const int kTileSizes[] = {4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32};
+// 36 and 40 run on CTA pairs only (a whole 40^3 spectrum exceeds one CTA's
+// shared memory): the big-kernel nets (k = 7, 9) waste less overlap-save work
+const int kTileSizes[] = {4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32, 36, 40};
 const int kNumTileSizes = sizeof(kTileSizes) / sizeof(int);
 
 int64_t tile_nwp(int T, int lw) {
@@ -860,6 +872,8 @@ int64_t tile_nwp(int T, int lw) {
     case 28: FN<28>(c, a, nblocks); break;                          \
     case 30: FN<30>(c, a, nblocks); break;                          \
     case 32: FN<32>(c, a, nblocks); break;                          \
+    case 36: FN<36>(c, a, nblocks); break;                          \
+    case 40: FN<40>(c, a, nblocks); break;                          \
     default: throw invalid("tile fft: unsupported tile size");      \
   }
 

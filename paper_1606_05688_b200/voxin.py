@@ -336,7 +336,7 @@ def conv_fft_tiled(input, params: ConvLayerParams, tile: int, tensor_cores: bool
     return out
 
 
-TILE_SIZES = (4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32)
+TILE_SIZES = (4, 6, 8, 10, 12, 16, 20, 24, 28, 30, 32, 36, 40)  # 36, 40: CTA pairs (k_tilefft.cu)
 
 
 def _pool(fn, input, p, P, ctx):

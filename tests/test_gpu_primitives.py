@@ -393,3 +393,24 @@ def test_conv_fft_pair_tile_contraction_kept(oracle, ctx, monkeypatch, fo):
     b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
     got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=True, ctx=ctx)
     assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
+
+
+@pytest.mark.parametrize("S,f,fo,n,T", [(2, 80, 80, 70, 32), (1, 16, 80, 60, 16), (1, 80, 16, 60, 16),
+                                        (4, 80, 80, 40, 16), (1, 8, 16, 40, 16), (1, 80, 80, 60, 40),
+                                        (2, 32, 48, 50, 36)])
+def test_conv_fft_tensor_cores_match_ffma_contraction(ctx, S, f, fo, n, T):
+    """The tcgen05 quad-tile contraction against the independent fp32 FFMA
+    contraction on the same transforms, at sizes where every CTA loops over
+    many tiles and both shared-memory rings wrap many times (a cross-proxy
+    race in the staged-X ring showed only here), incl. the pair-only T = 36/40."""
+    import torch
+    import paper_1606_05688_b200 as v
+    g = torch.Generator(device="cuda").manual_seed(S * 1000 + f + fo + n + T)
+    x = torch.rand((S, f, n, n, n), device="cuda", generator=g) * 2 - 1
+    w = (torch.rand((fo, f, 5, 5, 5), device="cuda", generator=g) * 2 - 1) * (3.0 / (f * 125)) ** 0.5
+    b = (torch.rand((fo,), device="cuda", generator=g) * 2 - 1) * 0.1
+    p = v.ConvLayerParams(w.contiguous(), b.contiguous(), "identity")
+    a = v.conv_fft_tiled(x, p, T, tensor_cores=False, ctx=ctx)
+    c = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
+    err = ((a - c).abs().max() / a.abs().max()).item()
+    assert err <= 1e-5, err
