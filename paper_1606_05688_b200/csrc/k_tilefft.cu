@@ -110,9 +110,10 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   // A0: real box -> slots (asynchronous 4-byte copies, zero outside the image).
   // Warp w owns x planes w, w + nwarps, ...; lane = z; rows advance by
   // pointer increments (no per-element index arithmetic).
-  {
+  // (T > 32: the z rows take two lane passes)
+  for (int zb = 0; zb < T; zb += 32) {
     constexpr int NWARPS = C::THREADS / 32;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = (tid & 31) + zb, warp = tid >> 5;
     const int gz = oz + lane;
     if (ox + T <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
       // interior box (the common case): no bounds tests, one LDGSTS per row
@@ -296,9 +297,9 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdT
   const float* img = a.src + (s * a.f + j) * a.img_stride;
   const int tid = threadIdx.x;
 
-  // A0: this CTA's planes (raw) -> slots
-  {
-    const int lane = tid & 31, warp = tid >> 5;
+  // A0: this CTA's planes (raw) -> slots (T > 32: two lane passes per z row)
+  for (int zb = 0; zb < T; zb += 32) {
+    const int lane = (tid & 31) + zb, warp = tid >> 5;
     const int gz = oz + lane;
     if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
       if (lane < T) {
@@ -538,9 +539,10 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
 
   // E: store of the crop, clipped to the output image: warp w owns x planes
   // w, w + nwarps, ...; lane = z; rows advance by pointer increments.
-  {
+  // (T > 32: the z rows take two lane passes)
+  for (int zb = 0; zb < T; zb += 32) {
     constexpr int NWARPS = C::THREADS / 32;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = (tid & 31) + zb, warp = tid >> 5;
     const int gx0 = tx * a.vx, gy0 = ty * a.vy, gz = tz * a.vz + lane;
     const bool zin = lane < a.vz && gz < a.onz;
     const int ylim = min(a.vy, a.ony - gy0);
@@ -717,9 +719,9 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
   }
   __syncthreads();
 
-  // E: store my crop planes, clipped to the output image
-  {
-    const int lane = tid & 31, warp = tid >> 5;
+  // E: store my crop planes, clipped to the output image (vz > 32: two lane passes)
+  for (int zb = 0; zb < T; zb += 32) {
+    const int lane = (tid & 31) + zb, warp = tid >> 5;
     const int gy0 = ty * a.vy, gz = tz * a.vz + lane;
     const bool zin = lane < a.vz && gz < a.onz;
     const int ylim = min(a.vy, a.ony - gy0);
