@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       }
       // the box may be refilled: order these generic-proxy reads before the
       // producer's next TMA (async-proxy) write into the slot
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // required: without it the refill races the reads
       mbar_arrive(&rfree[s]);
       if (a.prof) cb += clock64() - t1;
       t1 = a.prof ? clock64() : 0;
