@@ -183,7 +183,7 @@ def choose_patch(model, net, fov, budget_bytes, tuned, extent=0, quick=False):
     return (best[1], best[2]) if best else (None, None)
 
 
-def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm):
+def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm, per_layer=None):
     """sum over layers of max(F_l / P_fp32, B_l / P_hbm) with
     F_fft = 7.5 S (f+f') N^3 log2 N + 2.5 f f' N log2 N (k^2 + kN + N^2) + 8 S f f' #w,
     F_dir = 2 S f f' n'^3 k^3 (the cheaper conv per layer), MPF bytes
@@ -203,13 +203,18 @@ def layer_roofline(net_layers, e, fov, peak_fp32, peak_hbm):
                 + 8.0 * S * f * fo * nw
             F_dir = 2.0 * S * f * fo * no ** 3 * k ** 3
             B = 4.0 * (S * f * n ** 3 + S * fo * no ** 3 + f * fo * k ** 3 + fo)
-            total += max(min(F_fft, F_dir) / (peak_fp32 * 1e12), B / (peak_hbm * 1e9))
+            t = max(min(F_fft, F_dir) / (peak_fp32 * 1e12), B / (peak_hbm * 1e9))
+            total += t
+            if per_layer is not None:
+                per_layer.append(t)
             f, n = fo, no
         else:
             p = l[1][0]
             m = n // p
             B = 4.0 * S * f * (n ** 3 + p ** 3 * m ** 3)
             total += B / (peak_hbm * 1e9)
+            if per_layer is not None:
+                per_layer.append(B / (peak_hbm * 1e9))
             S *= p ** 3
             n = m
     return total
@@ -442,8 +447,10 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream())
     cache = bool(args.cache_spectra)
 
+    last = {}
+
     def step():
-        model.forward(x_dev, out=out_dev, conv_algos=algos, cache_spectra=cache)
+        last["rep"] = model.forward(x_dev, out=out_dev, conv_algos=algos, cache_spectra=cache)[1]
 
     for _ in range(args.warmup):
         step()
@@ -562,9 +569,17 @@ def main():
                               f"{ratio} (profiles/r1_ncu_summary.md)") if ratio else None
     roof["per_launch"] = {"flops": ds["flops"] / ds["launches"], "bytes": ds["bytes"] / ds["launches"],
                           "seconds": ds["seconds"] / ds["launches"]}
-    t_roof = layer_roofline(net.layers, e, fov, ffma_peak, peaks["hbm_gbs"])
+    roof_l = []
+    t_roof = layer_roofline(net.layers, e, fov, ffma_peak, peaks["hbm_gbs"], roof_l)
     step_s = elapsed / args.steps
+    meas_l = list(last["rep"].layer_seconds)
+    per_layer = [{"layer": i, "kind": ("conv" if l[0] == "conv" else "pool"),
+                  "plan": (f"{p.get('algo')}/T{p.get('T')}" if p["kind"] == "conv" else "mpf"),
+                  "measured_s": round(meas_l[i], 5) if i < len(meas_l) else None,
+                  "roofline_s": round(roof_l[i], 5)}
+                 for i, (l, p) in enumerate(zip(net.layers, plan))]
     net_roof = {"seconds": t_roof, "step_seconds": step_s, "frac": t_roof / step_s,
+                "per_layer": per_layer,
                 "definition": "SURVEY 8(d): sum_l max(F_l/P_fp32, B_l/P_hbm), F = cheaper of "
                               "whole-image pruned FFT and direct, P_fp32 = measured FFMA peak"}
 

@@ -302,3 +302,26 @@ def test_network_forward_rejects_nan_input(ctx):
     pm = v.Model(pnet, v.random_weights(pnet, 1), ctx)
     with pytest.raises(ValueError, match="NaN"):
         pm.forward(bad)
+
+
+def test_run_bench_csv_matches_the_reference_columns(tmp_path):
+    """tools/run_bench.py (the device `voxinfer bench`, proj/src/cli.cpp:225-280):
+    header and one row per admissible extent, memory columns in scalars, the
+    audited peak inside the model's band, layer times summing to the forward."""
+    import csv
+    import importlib.util
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    spec = importlib.util.spec_from_file_location("run_bench", root / "tools" / "run_bench.py")
+    rb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rb)
+    out = tmp_path / "bench.csv"
+    assert rb.main(["--net", "n337", "--min-extent", "92", "--max-extent", "108", "--csv", str(out)]) == 0
+    rows = list(csv.reader(open(out)))
+    assert rows[0][:5] == ["input_extent", "memory_model", "memory_audited", "voxels_per_sec", "seconds"]
+    assert rows[0][5:] == [f"layer{i}_ms" for i in range(len(rows[0]) - 5)]
+    assert len(rows) >= 3
+    for r in rows[1:]:
+        e, model, audited, vps, sec = int(r[0]), float(r[1]), float(r[2]), float(r[3]), float(r[4])
+        assert vps > 0 and sec > 0 and model > 0 and 0 < audited <= 1.15 * model
+        assert abs(sum(float(x) for x in r[5:]) * 1e-3 - sec) <= 0.25 * sec
