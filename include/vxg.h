@@ -79,6 +79,11 @@ int vxg_ctx_sync(vxg_ctx* ctx);
 int vxg_ctx_stream(vxg_ctx* ctx, void** cuda_stream);
 /* bytes currently held / high-water mark since the last reset */
 int vxg_ctx_memory(vxg_ctx* ctx, int64_t* current, int64_t* peak, int64_t* budget);
+/* Hand the network forward's cached arena block back to the device pool (it
+ * is kept between forwards so the next forward reuses it without remapping;
+ * the library drops it by itself when another allocation would not fit).
+ * No reference counterpart (the reference's host arenas are per call). */
+int vxg_ctx_trim(vxg_ctx* ctx);
 int vxg_ctx_reset_peak(vxg_ctx* ctx);
 /* number of kernels this context launched so far (for launch accounting) */
 int64_t vxg_ctx_launches(vxg_ctx* ctx);

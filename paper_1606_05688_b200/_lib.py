@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
         "vxg_ctx_create": (I, [I, I64, C.POINTER(P)]),
         "vxg_ctx_destroy": (I, [P]),
         "vxg_ctx_sync": (I, [P]),
+        "vxg_ctx_trim": (I, [P]),
         "vxg_ctx_stream": (I, [P, C.POINTER(P)]),
         "vxg_ctx_memory": (I, [P, A, A, A]),
         "vxg_ctx_reset_peak": (I, [P]),

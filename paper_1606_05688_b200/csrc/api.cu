@@ -11,6 +11,34 @@
 
 using namespace vxg;
 
+namespace vxg {
+namespace {
+std::mutex g_ctx_mu;
+std::vector<Ctx*> g_ctxs;
+}  // namespace
+
+void register_ctx(Ctx* c) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_ctxs.push_back(c);
+}
+
+void unregister_ctx(Ctx* c) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_ctxs.erase(std::remove(g_ctxs.begin(), g_ctxs.end(), c), g_ctxs.end());
+}
+
+void release_idle_memory(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  for (Ctx* o : g_ctxs) {
+    if (o->device != device) continue;
+    o->drop_held();
+    cudaStreamSynchronize(o->stream);
+    cudaMemPoolTrimTo(o->pool, 0);
+  }
+}
+}  // namespace vxg
+
+
 namespace {
 
 thread_local std::string g_err;
@@ -172,6 +200,8 @@ int vxg_ctx_create(int device, int64_t budget, vxg_ctx** out) {
       VXG_CUDA_CHECK(cudaMemPoolCreate(&c->pool, &pp));
       uint64_t thresh = UINT64_MAX;
       VXG_CUDA_CHECK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+      // other contexts' idle caches must not shrink this one's default budget
+      release_idle_memory(device);
       size_t free_b = 0, total_b = 0;
       VXG_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
       // default budget: the HBM free at creation minus a 2.5 GiB reserve (CUDA
@@ -187,6 +217,7 @@ int vxg_ctx_create(int device, int64_t budget, vxg_ctx** out) {
       delete c;
       throw;
     }
+    register_ctx(c);
     *out = reinterpret_cast<vxg_ctx*>(c);
   });
 }
@@ -194,12 +225,19 @@ int vxg_ctx_create(int device, int64_t budget, vxg_ctx** out) {
 int vxg_ctx_destroy(vxg_ctx* ctx) {
   return guard([&] {
     Ctx* c = ctx_of(ctx);
+    unregister_ctx(c);
+    c->held_busy = false;
+    c->drop_held();
     cudaStreamSynchronize(c->stream);
     if (c->d_flag) cudaFree(c->d_flag);
     cudaMemPoolDestroy(c->pool);
     cudaStreamDestroy(c->stream);
     delete c;
   });
+}
+
+int vxg_ctx_trim(vxg_ctx* ctx) {
+  return guard([&] { release_idle_memory(ctx_of(ctx)->device); });
 }
 
 int vxg_ctx_sync(vxg_ctx* ctx) {
@@ -735,7 +773,8 @@ int vxg_model_forward_ex(vxg_model* model, int mem, const float* input, int64_t 
       report->voxels = double(S) * double(p.dense.vol());
       report->seconds = ms * 1e-3;
       report->voxels_per_second = report->seconds > 0 ? report->voxels / report->seconds : 0;
-      report->device_peak = au.peak_scalars();
+      // the arena block is sized with headroom: audit what the forward used of it
+      report->device_peak = au.peak_scalars() - double(m.arena_slack) / 4.0;
       report->layers = std::min<int64_t>(64, int64_t(layer_s.size()));
       for (int64_t i = 0; i < report->layers; ++i) report->layer_seconds[i] = layer_s[size_t(i)];
     }

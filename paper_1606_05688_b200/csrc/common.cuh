@@ -74,10 +74,13 @@ struct Arena {
   i64 size = 0;
   std::map<i64, i64> free_;  // offset -> bytes
 
+  i64 used = 0, peak = 0;    // bytes handed out now / at most (the forward's audit)
+
   static constexpr i64 kAlign = 512;
   void reset(void* b, i64 n) {
     base = static_cast<char*>(b);
     size = n;
+    used = peak = 0;
     free_.clear();
     if (n > 0) free_[0] = n;
   }
@@ -90,10 +93,13 @@ struct Arena {
     const i64 off = best->first, len = best->second;
     free_.erase(best);
     if (len > bytes) free_[off + bytes] = len - bytes;
+    used += bytes;
+    if (used > peak) peak = used;
     return base + off;
   }
   void release(void* p, i64 bytes) {
     bytes = (bytes + kAlign - 1) / kAlign * kAlign;
+    used -= bytes;
     i64 off = static_cast<char*>(p) - base;
     auto next = free_.lower_bound(off);
     if (next != free_.end() && next->first == off + bytes) {
@@ -149,6 +155,14 @@ struct Ctx {
   std::vector<KRecord> krec;
   std::vector<cudaEvent_t> spare_events;
   Arena* arena = nullptr;  // set while a network forward runs (forward.cu)
+  // the forward's arena block, kept between forwards (a freed block of that
+  // size is split by the pool for the next forward's smaller requests, after
+  // which the arena no longer fits and the pool trims and remaps ~100 GB);
+  // charged against the budget only while a forward uses it, and handed back
+  // to the pool whenever a device allocation would not fit without it
+  void* held = nullptr;
+  i64 held_bytes = 0;
+  bool held_busy = false;
 
   // device bytes really obtainable now: free memory plus what the pool holds
   // unused (other users of the GPU -- e.g. torch tensors allocated after the
@@ -192,7 +206,24 @@ struct Ctx {
     current -= bytes;
   }
   void counted(i64 n = 1) { launches += n; }
+  // give the held arena block back to the pool (not while a forward uses it)
+  bool drop_held() {
+    if (!held || held_busy) return false;
+    cudaFreeAsync(held, stream);
+    held = nullptr;
+    held_bytes = 0;
+    held_bytes = 0;
+    return true;
+  }
 };
+
+// Contexts of this process (api.cu).  release_idle_memory hands the idle
+// cached device memory of every context on `device` -- held arena blocks and
+// the pools' unused reserves -- back to the driver: caches yield to any
+// allocation that would otherwise fail (another context's, or this one's).
+void register_ctx(Ctx* c);
+void unregister_ctx(Ctx* c);
+void release_idle_memory(int device);
 
 // Brackets one kernel launch with events when profiling is on.
 class KScope {
@@ -250,11 +281,16 @@ class DevBuf {
     }
     c->charge(bytes);
     void* p = nullptr;
+    if (trace_on() && c->arena)
+      std::fprintf(stderr, "[vxg] arena miss: %lld bytes from the pool (arena largest free %lld)\n",
+                   (long long)bytes, (long long)c->arena->largest());
     cudaError_t e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
     if (e == cudaErrorMemoryAllocation) {
+      if (trace_on()) std::fprintf(stderr, "[vxg] pool trim + remap for %lld bytes\n", (long long)bytes);
       // the pool keeps freed blocks mapped (release threshold = max); when none
       // of them fits, hand them back and map the request afresh
       cudaGetLastError();
+      release_idle_memory(c->device);
       cudaStreamSynchronize(c->stream);
       cudaMemPoolTrimTo(c->pool, 0);
       e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
@@ -281,6 +317,14 @@ class DevBuf {
   template <class T = float>
   T* as() const { return static_cast<T*>(p_); }
   void* get() const { return p_; }
+  // detach a pool allocation (the caller keeps it, and its budget charge)
+  void* release_ptr() {
+    void* q = p_;
+    p_ = nullptr;
+    n_ = 0;
+    c_ = nullptr;
+    return q;
+  }
   i64 bytes() const { return n_; }
 
  private:

@@ -484,29 +484,73 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
                     std::vector<double>* layer_seconds) {
   require(has_weights, "execute: planning-only model has no weights");
   EventTimer timer(c->stream, layer_seconds != nullptr);
-  DevBuf frags(c, p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1));
-  // kernel spectra first, so the group sizes below see their footprint
-  for (size_t li = 0; li < net.layers.size(); ++li)
-    if (net.layers[li].kind == 0 && p.choice[li].algo == VXG_CONV_FFT) {
-      const int h = timer.begin(li);
-      spectra_for(conv_index[li], p.choice[li].fft, cache);
-      timer.end(h);
+  auto all_spectra = [&] {
+    for (size_t li = 0; li < net.layers.size(); ++li)
+      if (net.layers[li].kind == 0 && p.choice[li].algo == VXG_CONV_FFT) {
+        const int h = timer.begin(li);
+        spectra_for(conv_index[li], p.choice[li].fft, cache);
+        timer.end(h);
+      }
+  };
+  // cached kernel spectra outlive the forward: they come from the pool, first
+  if (cache) all_spectra();
+  // Everything else -- the final fragment tensor, per-forward kernel spectra
+  // and their scratch, the recursion's activations and spectrum chunks --
+  // lives in one arena block.  The block is kept between forwards (Ctx::held):
+  // a freed block of that size is split by the pool for smaller requests,
+  // after which the next forward's block no longer fits and the pool trims
+  // and remaps ~100 GB; with every per-forward allocation inside it, the
+  // steady state never touches the pool.
+  const int64_t frags_bytes = p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1);
+  int64_t spec_bytes = 0, spec_scratch = 0;
+  if (!cache) {
+    int64_t f = net.fin;
+    for (size_t li = 0; li < net.layers.size(); ++li) {
+      const Layer& l = net.layers[li];
+      if (l.kind != 0) continue;
+      if (p.choice[li].algo == VXG_CONV_FFT) {
+        const FftPlan& fp = p.choice[li].fft;
+        spec_bytes += kernel_spectra_bytes(fp, f, l.fo) + 4096;
+        if (fp.tc) spec_scratch = std::max(spec_scratch, tile_nwp(fp.T, 16) * l.fo * f * 8 + 4096);
+      }
+      f = l.fo;
     }
-  // The recursion runs inside one arena block taken from the pool: the pool
-  // maps it once and hands the same block back every forward, and the
-  // arena's coalescing free list keeps the large spectrum chunks contiguous
-  // (a bare stream-ordered pool fragments across forwards and has to unmap
-  // and remap). A big job gets everything the budget leaves.
+  }
   {
     Sched sched(*this, p);
-    const int64_t avail0 = std::min(c->avail(), c->device_free() - (int64_t(512) << 20));
+    // the held block (if any) is ours to reuse: device memory in use but not
+    // charged while idle
+    const int64_t held = c->held_bytes;
+    const int64_t avail0 = std::min(c->avail(), c->device_free() + held - (int64_t(512) << 20));
     const int64_t in0 = sched.in_bytes(0, p.S);
     const int64_t top = sched.peak(0, 0, p.S, false) - in0;
+    const int64_t fixed = frags_bytes + 4096 + spec_bytes + spec_scratch;
     int64_t arena_bytes = int64_t(double(avail0) * 0.995);
-    if (top <= avail0) arena_bytes = std::min(arena_bytes, top + top / 4 + (int64_t(256) << 20));
-    DevBuf arena_buf(c, arena_bytes);
+    if (fixed + top <= avail0)
+      arena_bytes = std::min(arena_bytes, fixed + top + top / 4 + (int64_t(256) << 20));
+    if (trace_on())
+      std::fprintf(stderr, "[vxg] forward arena: need %lld held %lld avail %lld (budget left %lld, device %lld)\n",
+                   (long long)arena_bytes, (long long)held, (long long)avail0, (long long)c->avail(),
+                   (long long)c->device_free());
+    if (held >= arena_bytes && held <= avail0) {
+      arena_bytes = held;
+      c->charge(arena_bytes);
+    } else {
+      c->drop_held();
+      DevBuf blk(c, arena_bytes);  // charged
+      c->held = blk.release_ptr();
+      c->held_bytes = arena_bytes;
+    }
+    struct Busy {
+      Ctx* c;
+      ~Busy() {
+        c->held_busy = false;
+        c->release(c->held_bytes);  // idle: kept, not charged
+      }
+    } busy{c};
+    c->held_busy = true;
     Arena arena;
-    arena.reset(arena_buf.get(), arena_bytes);
+    arena.reset(c->held, arena_bytes);
     struct Scope {
       Ctx* c;
       ~Scope() {
@@ -518,20 +562,24 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
       std::lock_guard<std::mutex> lk(c->mu);
       c->arena = &arena;
     }
-    Runner r{*this, p, cache, Sched(*this, p), frags.as<float>(), 0, timer};
-    r.run(0, d_in, p.S, nullptr);
-  }
-  if (!cache) spectra.clear();  // stream-ordered frees: recomputed by the next forward
-  const size_t nwin = p.windows.size() / 3;
-  if (nwin == 0) {
+    DevBuf frags(c, frags_bytes);
+    if (!cache) all_spectra();  // in the arena, so the group sizes below see their footprint
+    {
+      Runner r{*this, p, cache, Sched(*this, p), frags.as<float>(), 0, timer};
+      r.run(0, d_in, p.S, nullptr);
+    }
+    if (!cache) spectra.clear();  // back to the arena (stream-ordered reuse only)
+    const size_t nwin = p.windows.size() / 3;
     const Shape& fin = p.shapes.back();
-    VXG_CUDA_CHECK(cudaMemcpy2DAsync(d_dense, size_t(fin.n.z) * 4, frags.get(), size_t(p.pz.back()) * 4,
-                                     size_t(fin.n.z) * 4, size_t(p.S * fin.f * fin.n.x * fin.n.y),
-                                     cudaMemcpyDeviceToDevice, c->stream));
-  } else {
-    const Shape& fin = p.shapes.back();
-    launch_recombine(c, frags.as<float>(), p.S * p.alpha, 0, fin.f, fin.n, p.windows.data(),
-                     int(nwin), d_dense, p.S, p.pz.back());
+    if (nwin == 0) {
+      VXG_CUDA_CHECK(cudaMemcpy2DAsync(d_dense, size_t(fin.n.z) * 4, frags.get(), size_t(p.pz.back()) * 4,
+                                       size_t(fin.n.z) * 4, size_t(p.S * fin.f * fin.n.x * fin.n.y),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      launch_recombine(c, frags.as<float>(), p.S * p.alpha, 0, fin.f, fin.n, p.windows.data(),
+                       int(nwin), d_dense, p.S, p.pz.back());
+    }
+    arena_slack = arena_bytes - arena.peak;
   }
   timer.collect(layer_seconds, net.layers.size());
 }

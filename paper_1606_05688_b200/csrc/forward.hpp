@@ -51,6 +51,7 @@ struct Model {
   std::map<std::pair<int, int>, DevBuf> spectra;  // (conv ordinal, T) -> kernel spectra
   std::map<int, LayerCosts> measured;             // conv ordinal -> measured costs
   double pool_elem = -1;                          // measured MPF seconds per input element
+  int64_t arena_slack = 0;  // last forward: arena block bytes it never used (not in its audit)
 
   bool has_weights = true;  // false: a planning-only model (plan / plan_bytes)
 

@@ -101,6 +101,11 @@ class Context:
     def sync(self):
         check(lib().vxg_ctx_sync(self._p))
 
+    def trim(self):
+        """Give the forward's cached arena block and the pool's free memory back
+        to the device (vxg_ctx_trim)."""
+        check(lib().vxg_ctx_trim(self._p))
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(lib().vxg_ctx_stream(self._p, C.byref(s)))
