@@ -466,18 +466,23 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows)
   const int64_t in = p.S * entry_bytes(p, 0);
   const int64_t frags = p.S * p.alpha * entry_bytes(p, p.shapes.size() - 1);
   const int64_t dense = p.S * p.f_out * p.dense.vol() * 4;
-  int64_t spectra_bytes = 0;
+  int64_t spectra_bytes = 0, scratch = 0;
   (void)cache;  // spectra are resident for the whole forward either way
   {
     int64_t f = net.fin;
     for (size_t li = 0; li < net.layers.size(); ++li) {
       const Layer& l = net.layers[li];
       if (l.kind != 0) continue;
-      if (p.choice[li].algo == VXG_CONV_FFT) spectra_bytes += kernel_spectra_bytes(p.choice[li].fft, f, l.fo);
+      if (p.choice[li].algo == VXG_CONV_FFT) {
+        const FftPlan& fp = p.choice[li].fft;
+        spectra_bytes += kernel_spectra_bytes(fp, f, l.fo);
+        // raw spectra before the tensor-core split (transient, one layer at a time)
+        if (fp.tc) scratch = std::max(scratch, tile_nwp(fp.T, 16) * l.fo * f * 8);
+      }
       f = l.fo;
     }
   }
-  return frags + dense + spectra_bytes + std::max(in, s.peak(t, 0, p.S, false));
+  return frags + dense + spectra_bytes + scratch + std::max(in, s.peak(t, 0, p.S, false));
 }
 
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
