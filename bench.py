@@ -599,7 +599,7 @@ def main():
                                 f"measured (vxg_model_tune, {t_tune:.1f} s before the timed region)")),
                    "planned_step_s": round(sum(l["seconds"] for l in plan), 4),
                    "layers": " ".join(
-                       (f"L{l['layer']}:{l['algo']}" + (f"/T{l['T']}" + ("/tc" if l['tc'] else "/ffma")
+                       (f"L{l['layer']}:{l['algo']}" + (f"/T{l['T']}" + (("/tc" if l.get('tc_tiles') != "pair" else "/tcp") if l['tc'] else "/ffma")
                                                           if l['algo'] == 'fft' else ""))
                        if l["kind"] == "conv" else f"L{l['layer']}:mpf" for l in plan),
                    "l2": "inputs and activations >> 126 MB L2 (no flush needed)"},

@@ -892,7 +892,7 @@ int vxg_model_plan_info(vxg_model* model, int64_t S, const int64_t e[3], const i
       o[1] = conv ? ch.algo : -1;
       o[2] = fft ? ch.fft.T : 0;
       o[3] = fft ? ch.fft.tiles : 0;
-      o[4] = fft && ch.fft.tc ? 1 : 0;
+      o[4] = fft && ch.fft.tc ? (ch.fft.quad ? 1 : 2) : 0;  // 1: quad tiles, 2: pair tiles
       o[5] = ch.measured ? 1 : 0;
       o[6] = int64_t(ch.seconds * 1e9);
     }
@@ -916,7 +916,7 @@ int vxg_model_plan_ex(vxg_model* model, int64_t S, const int64_t e[3], const int
         o[1] = conv ? ch.algo : p.pool_mode[li];
         o[2] = fft ? ch.fft.T : 0;
         o[3] = fft ? ch.fft.tiles : 0;
-        o[4] = fft && ch.fft.tc ? 1 : 0;
+        o[4] = fft && ch.fft.tc ? (ch.fft.quad ? 1 : 2) : 0;  // 1: quad tiles, 2: pair tiles
         o[5] = ch.measured ? 1 : 0;
         o[6] = int64_t(ch.seconds * 1e9);
         o[7] = 0;

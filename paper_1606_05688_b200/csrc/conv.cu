@@ -76,6 +76,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.tiles = p.nt.vol();
     p.lw = 16;
     p.tc = tc;
+    p.quad = tc_quad_enabled();
     // measured wins (other T <= 32: one CTA is as fast); T >= 36 runs on pairs only
     p.pair = ((T == 32 || T == 24) && tile_pair_enabled()) || T >= 36;
     p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 36;
@@ -101,6 +102,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   FftPlan p = plan_fft(n, k, f, fo, S, T);
   if (p.T != T) throw invalid("conv fft: unsupported tile size");
   p.tc = tc && cgemm_tc_supported(f, fo);
+  p.quad = tc_quad_enabled();
   p.pair = pair && T >= 24;  // tests: every pair-capable size
   p.inv_pair = pair && T >= 24;  // tests: every pair-capable size
   p.lw = 16;
@@ -110,13 +112,13 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
 }
 
 int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo) {
-  if (plan.tc) return tc_wsplit_bytes(plan.nwp / 2, f, fo);
+  if (plan.tc) return tc_wsplit_bytes(plan.nwp / 2, f, fo, plan.quad);
   return plan.nwp * fo * f * 8;
 }
 
 // tc: the raw spectra go through a scratch buffer and are stored pre-split
 // for the tensor cores (tc_wsplit); otherwise raw into `out`.
-void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, int64_t f, V3 k,
+void compute_kernel_spectra(Ctx* c, int T, bool tc, bool quad, const float* w, int64_t fo, int64_t f, V3 k,
                             float2* out) {
   DevBuf raw;
   float2* dst = out;
@@ -140,7 +142,7 @@ void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, 
   a.kind = VXG_K_KSPEC;
   a.lw = 16;
   launch_tile_fwd(c, T, a, fo * f);
-  if (tc) tc_wsplit(c, dst, out, tile_nwp(T, 16) / 2, f, fo);
+  if (tc) tc_wsplit(c, dst, out, tile_nwp(T, 16) / 2, f, fo, quad);
 }
 
 int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, const float* w,
@@ -154,7 +156,7 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
   DevBuf wbuf;
   if (!wspec) {
     wbuf.alloc(c, kernel_spectra_bytes(plan, f, fo));
-    compute_kernel_spectra(c, T, plan.tc, w, fo, f, k, wbuf.as<float2>());
+    compute_kernel_spectra(c, T, plan.tc, plan.quad, w, fo, f, k, wbuf.as<float2>());
     wspec = wbuf.as<float2>();
   }
   const int64_t M = S * plan.tiles;
@@ -202,6 +204,7 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
     ga.fo = int(fo);
     ga.T = T;
     ga.ypair = plan.ylw == 2 ? 1 : 0;
+    ga.quad = plan.quad ? 1 : 0;
     if (plan.tc)
       launch_cgemm_tc(c, ga, plan.nwp / 2);
     else

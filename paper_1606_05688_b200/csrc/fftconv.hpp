@@ -59,6 +59,7 @@ struct GemmArgs {
   long long* prof = nullptr; // VXG_TC_PROF: per-CTA role cycle counters
   int dbg = 0;               // VXG_TC_DBG experiment switches (results invalid when set)
   int ypair = 0;             // Y pair-major ([w/2][row][map][2]) instead of line-major
+  int quad = 1;              // tensor cores: quad-frequency tiles (k_cgemm_q.cu), else pairs
 };
 
 extern const int kTileSizes[];
@@ -75,8 +76,9 @@ void launch_cgemm(Ctx* c, const GemmArgs& a, int64_t nwb);          // FFMA, lw 
 bool cgemm_tc_supported(int64_t f, int64_t fo);
 void launch_cgemm_tc(Ctx* c, const GemmArgs& a, int64_t npairs);    // tcgen05, lw = 2
 // pre-split (tf32 hi/lo, UMMA layout) kernel spectra for the tensor-core path
-int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
-void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
+// (quad: the layout k_cgemm_q.cu reads; else k_cgemm_tc.cu's)
+int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo, bool quad);
+void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo, bool quad);
 // quad-frequency tiles (k_cgemm_q.cu, the default tensor-core contraction):
 // sector-complete epilogue stores, pass-split accumulators
 bool tc_quad_enabled();
@@ -95,6 +97,8 @@ struct FftPlan {
   int ylw = 16;      // Y chunk width: 2 = pair-major (tcgen05 epilogue writes whole lines,
                      // the CTA-pair inverse gathers its x lines by TMA)
   bool tc = false;   // tcgen05 3xTF32 contraction (else fp32 FFMA)
+  bool quad = true;  // tcgen05 tile shape: 4 frequencies x half the maps (k_cgemm_q.cu) or
+                     // 2 frequencies x all maps (k_cgemm_tc.cu); the measured planner picks
   bool pair = false;     // forward tile transform on a CTA pair (T >= 24)
   bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
@@ -106,7 +110,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced = 0)
 FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, bool tc, bool pair);
 
 // Device kernel spectra of one layer for tile size T: [w/lw][fo][f][lw], scaled 1/T^3.
-void compute_kernel_spectra(Ctx* c, int T, bool tc, const float* w, int64_t fo, int64_t f, V3 k,
+void compute_kernel_spectra(Ctx* c, int T, bool tc, bool quad, const float* w, int64_t fo, int64_t f, V3 k,
                             float2* out);
 // bytes of one layer's device kernel spectra in the layout plan.lw selects
 int64_t kernel_spectra_bytes(const FftPlan& plan, int64_t f, int64_t fo);

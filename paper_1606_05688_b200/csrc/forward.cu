@@ -127,7 +127,8 @@ ForwardPlan Model::plan(int64_t S, V3 e, const int* conv_algos, const int* pool_
         FftPlan best;
         double best_s = 1e300;
         for (const auto& kv : mit->second.fft) {
-          FftPlan q = plan_fft(in.n, l.ext, in.f, l.fo, B, kv.first);
+          FftPlan q = plan_fft(in.n, l.ext, in.f, l.fo, B, kv.first & kTuneT);
+          if (kv.first & kTunePairTiles) q.quad = false;
           q.cost = kv.second.first + kv.second.second * double(B) * double(q.tiles);
           if (q.cost < best_s) {
             best_s = q.cost;
@@ -436,7 +437,7 @@ struct Runner {
 // they are dropped at the end of the forward, so every forward recomputes them.
 const float2* Model::spectra_for(int ci, const FftPlan& plan, bool /*cache*/) {
   const int T = plan.T;
-  auto key = std::make_pair(ci, (T << 8) | (plan.tc ? 1 : 0));
+  auto key = std::make_pair(ci, (T << 8) | (plan.tc ? 1 : 0) | (plan.tc && plan.quad ? 2 : 0));
   auto it = spectra.find(key);
   if (it != spectra.end()) return it->second.as<float2>();
   int64_t f = net.fin;
@@ -445,7 +446,7 @@ const float2* Model::spectra_for(int ci, const FftPlan& plan, bool /*cache*/) {
     if (l.kind != 0) continue;
     if (conv_index[li] == ci) {
       DevBuf b(c, kernel_spectra_bytes(plan, f, l.fo));
-      compute_kernel_spectra(c, T, plan.tc, kern[size_t(ci)].as<float>(), l.fo, f, l.ext,
+      compute_kernel_spectra(c, T, plan.tc, plan.quad, kern[size_t(ci)].as<float>(), l.fo, f, l.ext,
                              b.as<float2>());
       auto res = spectra.emplace(key, std::move(b));
       return res.first->second.as<float2>();
@@ -709,18 +710,24 @@ void Model::tune(int64_t S, V3 e) {
       DevBuf x(c, S2 * f * ns.vol() * 4);
       DevBuf y(c, S2 * fo * nso.vol() * 4);
       fill_sample(c, x.as<float>(), S2 * f * ns.vol(), 12345u + uint32_t(T));
-      DevBuf ws(c, kernel_spectra_bytes(fp, f, fo));
-      compute_kernel_spectra(c, T, fp.tc, w, fo, f, k, ws.as<float2>());
-      double t[2];
-      const int64_t Ss[2] = {S1, S2};
-      for (int q = 0; q < 2; ++q)
-        t[q] = time_on_stream(c, [&] {
-          conv_fft_device(c, x.as<float>(), Ss[q], f, ns, w, fo, k, b, l.relu, y.as<float>(), fp,
-                          ws.as<float2>(), 0);
-        }, 2);
-      const double rows1 = double(S1 * fp.tiles), rows2 = double(S2 * fp.tiles);
-      const double per_row = std::max(0.0, (t[1] - t[0]) / (rows2 - rows1));
-      lc.fft[T] = {std::max(0.0, t[0] - per_row * rows1), per_row};
+      // tensor-core layers: both tile shapes (quad frequencies x half the
+      // maps, pairs x all maps) -- which wins depends on T and the row count
+      const int variants = (fp.tc && fp.quad) ? 2 : 1;
+      for (int vq = 0; vq < variants; ++vq) {
+        fp.quad = fp.tc && fp.quad && vq == 0;
+        DevBuf ws(c, kernel_spectra_bytes(fp, f, fo));
+        compute_kernel_spectra(c, T, fp.tc, fp.quad, w, fo, f, k, ws.as<float2>());
+        double t[2];
+        const int64_t Ss[2] = {S1, S2};
+        for (int q = 0; q < 2; ++q)
+          t[q] = time_on_stream(c, [&] {
+            conv_fft_device(c, x.as<float>(), Ss[q], f, ns, w, fo, k, b, l.relu, y.as<float>(), fp,
+                            ws.as<float2>(), 0);
+          }, 2);
+        const double rows1 = double(S1 * fp.tiles), rows2 = double(S2 * fp.tiles);
+        const double per_row = std::max(0.0, (t[1] - t[0]) / (rows2 - rows1));
+        lc.fft[T | (vq ? kTunePairTiles : 0)] = {std::max(0.0, t[0] - per_row * rows1), per_row};
+      }
     }
     // direct convolution, where it might compete
     {
@@ -729,7 +736,7 @@ void Model::tune(int64_t S, V3 e) {
       const double dmodel = 2.0 * double(f) * fo * double(no.vol()) * double(k.vol()) / 40e12;
       double best_fft = 1e300;
       for (const auto& kv : lc.fft) {
-        const FftPlan q = plan_fft(in.n, k, f, fo, 1, kv.first);
+        const FftPlan q = plan_fft(in.n, k, f, fo, 1, kv.first & kTuneT);
         best_fft = std::min(best_fft, kv.second.first + kv.second.second * double(q.tiles));
       }
       if (ch.algo == VXG_CONV_DIRECT || dmodel < 4.0 * best_fft) {
@@ -760,7 +767,8 @@ void Model::tune(int64_t S, V3 e) {
       std::fprintf(stderr, "[vxg] tune layer %zu (f=%lld fo=%lld k=%lld):", li, (long long)f,
                    (long long)fo, (long long)k.x);
       for (const auto& kv : lc.fft)
-        std::fprintf(stderr, " T%d %.3gms+%.3gns/row", kv.first, kv.second.first * 1e3, kv.second.second * 1e9);
+        std::fprintf(stderr, " T%d%s %.3gms+%.3gns/row", kv.first & kTuneT, (kv.first & kTunePairTiles) ? "p" : "",
+                     kv.second.first * 1e3, kv.second.second * 1e9);
       if (lc.direct_vox > 0) std::fprintf(stderr, " direct %.3gns/vox", lc.direct_vox * 1e9);
       std::fprintf(stderr, "\n");
     }

@@ -36,8 +36,13 @@ struct ForwardPlan {
 // Measured per-layer costs (Model::tune): seconds per spectrum row of the
 // tiled FFT convolution for each tile size, seconds per output voxel of the
 // direct convolution; keyed by the layer's (f, fo, k).
+// LayerCosts::fft keys: tile size T, | kTunePairTiles for the pair-tile
+// tensor-core contraction (k_cgemm_tc.cu) instead of the quad tiles
+constexpr int kTuneT = 0xFFFF;
+constexpr int kTunePairTiles = 1 << 16;
+
 struct LayerCosts {
-  // T -> {fixed seconds per launch, seconds per (batch, tile) row}: fitted
+  // key -> {fixed seconds per launch, seconds per (batch, tile) row}: fitted
   // from two sample sizes (the fixed part is mostly the kernel-spectrum stream)
   std::map<int, std::pair<double, double>> fft;
   double direct_vox = -1;         // seconds per output voxel (all maps), < 0: not measured

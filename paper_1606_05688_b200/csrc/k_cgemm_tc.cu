@@ -441,8 +441,8 @@ bool cgemm_tc_supported(int64_t f, int64_t fo) {
   return f % TC_KC == 0 && f >= TC_KC && fo % 16 == 0 && fo >= 16 && fo <= 80;
 }
 
-int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
-  if (tc_quad_enabled()) return q_wsplit_bytes(npairs, f, fo);
+int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo, bool quad) {
+  if (quad) return q_wsplit_bytes(npairs, f, fo);
   return npairs * (f / TC_KC) * 8 * fo * TC_KC * 4;
 }
 
@@ -456,8 +456,8 @@ int64_t tc_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
     default: throw invalid("cgemm_tc: unsupported output map count"); \
   }
 
-void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo) {
-  if (tc_quad_enabled()) return q_wsplit(c, raw, out, npairs, f, fo);
+void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo, bool quad) {
+  if (quad) return q_wsplit(c, raw, out, npairs, f, fo);
   KScope ks(c, VXG_K_KSPEC, 0.0, double(npairs) * f * fo * (16.0 + 32.0));
 #define VXG_WS(F) wsplit_t<F>(c, raw, out, npairs, int(f))
   VXG_TC_SWITCH(VXG_WS)
@@ -466,7 +466,7 @@ void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, 
 
 // Y[w/16][row][fo][16] = X[w/16][row][f][16] . W (pre-split by tc_wsplit)
 void launch_cgemm_tc(Ctx* c, const GemmArgs& a, int64_t npairs) {
-  if (tc_quad_enabled() && !a.ypair) return launch_cgemm_q(c, a, npairs);
+  if (a.quad && !a.ypair) return launch_cgemm_q(c, a, npairs);
   const double nw = double(a.T) * a.T * (a.T / 2 + 1);
   KScope ks(c, VXG_K_CGEMM, 8.0 * double(a.M) * a.f * a.fo * nw,
             8.0 * nw * (double(a.M) * a.f + double(a.M) * a.fo + double(a.f) * a.fo));

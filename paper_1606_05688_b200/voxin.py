@@ -662,7 +662,8 @@ class Model:
             k, a, T, tiles, tc, meas, ns = buf[7 * i:7 * i + 7]
             if k == 0:
                 out.append({"layer": i, "kind": "conv", "algo": algo.get(a, str(a)), "T": T,
-                            "tiles": tiles, "tc": bool(tc), "measured": bool(meas), "seconds": ns * 1e-9})
+                            "tiles": tiles, "tc": bool(tc), "tc_tiles": {1: "quad", 2: "pair"}.get(int(tc)),
+                            "measured": bool(meas), "seconds": ns * 1e-9})
             else:
                 out.append({"layer": i, "kind": "pool", "seconds": ns * 1e-9})
         return out
