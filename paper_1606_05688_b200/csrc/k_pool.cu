@@ -377,25 +377,29 @@ __device__ __forceinline__ int64_t frag_term(const RecGeom& g, int64_t off, int 
   return b;
 }
 
+// Persistent over dense rows (s, fm, dx, dy): one block per row made 16M tiny
+// blocks at n726's 80 x 453^2 rows (~0.5 TB/s); each block now sets up its
+// fragment-offset table once and streams many rows.
 __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict__ frag,
-                                                        float* __restrict__ dense, RecGeom g) {
+                                                        float* __restrict__ dense, RecGeom g, int64_t rows) {
   __shared__ int64_t ztab[256];  // fragment-offset term per dz % sz (sz <= 256)
-  const int64_t row = blockIdx.x;  // (s, fm, dx, dy)
-  const int64_t dy = row % g.dy;
-  const int64_t dx = (row / g.dy) % g.dx;
-  const int64_t sf = row / (g.dy * g.dx);
-  const int64_t fm = sf % g.f, s = sf / g.f;
   for (int o = threadIdx.x; o < g.sz; o += blockDim.x) ztab[o] = frag_term(g, o, 2);
   __syncthreads();
   const int64_t nel = g.nx * g.ny * g.fpz;
-  const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
-  const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz;
-  float* dst = dense + row * g.dz;
   const int sz = int(g.sz);
   const int64_t fstride = g.f * nel;
-  for (int dz = threadIdx.x; dz < g.dz; dz += blockDim.x) {
-    const int oz = dz % sz;
-    dst[dz] = __ldg(src + (bxy + ztab[oz]) * fstride + dz / sz);
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t dy = row % g.dy;
+    const int64_t dx = (row / g.dy) % g.dx;
+    const int64_t sf = row / (g.dy * g.dx);
+    const int64_t fm = sf % g.f, s = sf / g.f;
+    const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
+    const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz;
+    float* dst = dense + row * g.dz;
+    for (int dz = threadIdx.x; dz < g.dz; dz += blockDim.x) {
+      const int oz = dz % sz;
+      dst[dz] = __ldg(src + (bxy + ztab[oz]) * fstride + dz / sz);
+    }
   }
 }
 
@@ -481,8 +485,7 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
   KScope ks(c, VXG_K_RECOMBINE, 0.0, 8.0 * double(total));
   require(g.sz <= 256, "recombine: z stride product above 256");
   const int64_t rows = S0 * f * g.dx * g.dy;
-  require(rows < (int64_t(1) << 31), "recombine: too many dense rows");
-  recombine_kernel<<<unsigned(rows), 256, 0, c->stream>>>(frag, dense, g);
+  recombine_kernel<<<grid_for(rows, 1, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(frag, dense, g, rows);
   c->counted();
   check_launch("recombine_kernel");
 }

@@ -162,17 +162,12 @@ def run_tiles(forward: Callable, volume, tiles: Iterable[Tile], out=None,
     blocks = {}
     todo = [t for t in tiles if not (done is not None and t.index in done)]
     step = batch if forward_many is not None else 1
-    for b0 in range(0, len(todo), step):
-        grp = todo[b0:b0 + step]
-        t0 = time.perf_counter()
-        crops = [_crop(volume, t) for t in grp]
-        t1 = time.perf_counter()
-        same = all(t.in_extent == grp[0].in_extent for t in grp)
-        if forward_many is not None and same and len(grp) > 1:
-            results = forward_many(crops)
-        else:
-            results = [forward(c) for c in crops]
-        t2 = time.perf_counter()
+    groups = [todo[b0:b0 + step] for b0 in range(0, len(todo), step)]
+
+    def make_crops(grp):
+        return [_crop(volume, t) for t in grp]
+
+    def write(grp, results):
         for t, r in zip(grp, results):
             block = _owned(np.asarray(r), t)
             if out is not None:
@@ -181,9 +176,38 @@ def run_tiles(forward: Callable, volume, tiles: Iterable[Tile], out=None,
                 blocks[t.index] = block
             if done is not None:
                 done.add(t.index)
-        if timings is not None:
-            timings.append({"tiles": [t.index for t in grp], "crop_s": t1 - t0, "forward_s": t2 - t1,
-                            "write_s": time.perf_counter() - t2})
+
+    # three-stage pipeline: the next batch's crops and the previous batch's
+    # writes run on helper threads while the current batch is on the GPU (the
+    # forward is a ctypes call, which releases the GIL, as do numpy's copies)
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=2) as ex:
+        nxt = ex.submit(make_crops, groups[0]) if groups else None
+        pending = None
+        for i, grp in enumerate(groups):
+            t0 = time.perf_counter()
+            crops = nxt.result()
+            if i + 1 < len(groups):
+                nxt = ex.submit(make_crops, groups[i + 1])
+            t1 = time.perf_counter()
+            same = all(t.in_extent == grp[0].in_extent for t in grp)
+            if forward_many is not None and same and len(grp) > 1:
+                results = forward_many(crops)
+            else:
+                results = [forward(c) for c in crops]
+            t2 = time.perf_counter()
+            if pending is not None:
+                pending.result()
+            pending = ex.submit(write, grp, results)
+            if timings is not None:
+                # crop_s / write_s: time the GPU loop waited on the helper threads
+                timings.append({"tiles": [t.index for t in grp], "crop_s": t1 - t0, "forward_s": t2 - t1,
+                                "write_s": time.perf_counter() - t2})
+        if pending is not None:
+            t3 = time.perf_counter()
+            pending.result()
+            if timings:
+                timings[-1]["write_s"] += time.perf_counter() - t3
     return blocks
 
 
