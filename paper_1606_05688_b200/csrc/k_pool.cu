@@ -377,9 +377,10 @@ __device__ __forceinline__ int64_t frag_term(const RecGeom& g, int64_t off, int 
   return b;
 }
 
-// Persistent over dense rows (s, fm, dx, dy): one block per row made 16M tiny
-// blocks at n726's 80 x 453^2 rows (~0.5 TB/s); each block now sets up its
-// fragment-offset table once and streams many rows.
+// Persistent over groups of RG dense rows (s, fm, dx, dy): each thread keeps
+// RG independent fragment loads in flight (one per row) -- one row per block
+// and one load per thread left ~1 TB/s of requests in flight.
+constexpr int RG = 4;
 __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict__ frag,
                                                         float* __restrict__ dense, RecGeom g, int64_t rows) {
   __shared__ int64_t ztab[256];  // fragment-offset term per dz % sz (sz <= 256)
@@ -388,17 +389,31 @@ __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict_
   const int64_t nel = g.nx * g.ny * g.fpz;
   const int sz = int(g.sz);
   const int64_t fstride = g.f * nel;
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const int64_t dy = row % g.dy;
-    const int64_t dx = (row / g.dy) % g.dx;
-    const int64_t sf = row / (g.dy * g.dx);
-    const int64_t fm = sf % g.f, s = sf / g.f;
-    const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
-    const float* src = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz;
-    float* dst = dense + row * g.dz;
+  for (int64_t row0 = int64_t(blockIdx.x) * RG; row0 < rows; row0 += int64_t(gridDim.x) * RG) {
+    const float* src[RG];
+    float* dst[RG];
+    bool ok[RG];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      const int64_t row = row0 + r;
+      ok[r] = row < rows;
+      const int64_t rr = ok[r] ? row : row0;
+      const int64_t dy = rr % g.dy;
+      const int64_t dx = (rr / g.dy) % g.dx;
+      const int64_t sf = rr / (g.dy * g.dx);
+      const int64_t fm = sf % g.f, s = sf / g.f;
+      const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
+      src[r] = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz + bxy * fstride;
+      dst[r] = dense + rr * g.dz;
+    }
     for (int dz = threadIdx.x; dz < g.dz; dz += blockDim.x) {
-      const int oz = dz % sz;
-      dst[dz] = __ldg(src + (bxy + ztab[oz]) * fstride + dz / sz);
+      const int64_t off = ztab[dz % sz] * fstride + dz / sz;
+      float v[RG];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) v[r] = ok[r] ? __ldg(src[r] + off) : 0.f;
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        if (ok[r]) dst[r][dz] = v[r];
     }
   }
 }
@@ -485,7 +500,7 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
   KScope ks(c, VXG_K_RECOMBINE, 0.0, 8.0 * double(total));
   require(g.sz <= 256, "recombine: z stride product above 256");
   const int64_t rows = S0 * f * g.dx * g.dy;
-  recombine_kernel<<<grid_for(rows, 1, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(frag, dense, g, rows);
+  recombine_kernel<<<grid_for(rows, RG, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(frag, dense, g, rows);
   c->counted();
   check_launch("recombine_kernel");
 }

@@ -414,3 +414,22 @@ def test_conv_fft_tensor_cores_match_ffma_contraction(ctx, S, f, fo, n, T):
     c = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
     err = ((a - c).abs().max() / a.abs().max()).item()
     assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("T", [24, 32])
+def test_conv_fft_fused_z_load_vs_oracle(oracle, ctx, T):
+    """The CTA-pair forward transform's fused path (interior boxes with 16-byte
+    aligned z rows load their rows straight into registers for the z r2c):
+    z extent a multiple of 4 and V = T - 4 a multiple of 4 select it, boundary
+    boxes take the staged path -- both against the C oracle."""
+    import paper_1606_05688_b200 as v
+    S, f, fo, k = 2, 16, 16, (5, 5, 5)
+    n = (2 * (T - 4) + 9, 2 * (T - 4) + 6, 3 * (T - 4) + 4)
+    assert n[2] % 4 == 0
+    rng = np.random.default_rng(T)
+    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 125))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    got = v.conv_fft_tiled(_cuda(x), v.ConvLayerParams(_cuda(w), _cuda(b), "relu"), T, tensor_cores=True,
+                           cta_pair=True, ctx=ctx)
+    assert rel_error(got.cpu().numpy(), oracle.conv(x, w, b, True)) <= 1e-4
