@@ -24,7 +24,6 @@ struct FwdTileArgs {
   int kind = VXG_K_TILE_FWD; // instrumentation family (images or kernel spectra)
   int lw = 16;               // frequencies per contiguous chunk (16: FFMA path, 2: tensor cores)
   bool pair = false;         // CTA-pair transform (tile_fwd_pair_kernel) where available
-  int dbg_fz = 0;            // VXG_NO_FZ=1: stage the box through shared memory (A/B timing)
 };
 
 struct InvTileArgs {

@@ -362,11 +362,9 @@ struct RecGeom {
   int64_t scale[8];          // fragments per unit of window w's index
 };
 
-// Row-wise gather: one CTA per dense row (s, map, dx, dy).  The fragment a
-// dense voxel comes from is b(s) + fx(dx) + fy(dy) + fz(dz % sz) with each
-// term a sum over the windows (recombine_fragments' index decomposition,
-// layers.hpp:493-517); the z term is tabulated once per CTA in shared memory,
-// so the inner loop is one table read, one gather and one coalesced store.
+// The fragment a dense voxel comes from is b(s) + fx(dx) + fy(dy) + fz(dz % sz)
+// with each term a sum over the windows (recombine_fragments' index
+// decomposition, layers.hpp:493-517).
 __device__ __forceinline__ int64_t frag_term(const RecGeom& g, int64_t off, int axis) {
   int64_t b = 0;
   for (int w = 0; w < g.nwin; ++w) {
@@ -377,44 +375,47 @@ __device__ __forceinline__ int64_t frag_term(const RecGeom& g, int64_t off, int 
   return b;
 }
 
-// Persistent over groups of RG dense rows (s, fm, dx, dy): each thread keeps
-// RG independent fragment loads in flight (one per row) -- one row per block
-// and one load per thread left ~1 TB/s of requests in flight.
-constexpr int RG = 4;
+// Persistent over groups of rg dense rows (s, fm, dx, dy).  A dense z row
+// interleaves sz fragment rows (dense z = sz * zf + oz); gathering it element
+// by element made every warp load touch sz fragment rows hundreds of MB apart
+// (~0.5 TB/s).  Here the sz fragment rows of rg dense rows are read whole
+// (coalesced) into shared memory in dense order, then the dense rows are
+// written whole.
+constexpr int REC_SMEM_FLOATS = 8192;  // rg * dz floats (dz <= 8192)
+constexpr int REC_MAX_PAIRS = 1024;    // rg * sz fragment rows per group
+
 __global__ void __launch_bounds__(256) recombine_kernel(const float* __restrict__ frag,
-                                                        float* __restrict__ dense, RecGeom g, int64_t rows) {
-  __shared__ int64_t ztab[256];  // fragment-offset term per dz % sz (sz <= 256)
-  for (int o = threadIdx.x; o < g.sz; o += blockDim.x) ztab[o] = frag_term(g, o, 2);
-  __syncthreads();
+                                                        float* __restrict__ dense, RecGeom g, int64_t rows,
+                                                        int rg) {
+  __shared__ float buf[REC_SMEM_FLOATS];
+  __shared__ const float* ptab[REC_MAX_PAIRS];  // (row in group, oz) -> fragment row
   const int64_t nel = g.nx * g.ny * g.fpz;
-  const int sz = int(g.sz);
+  const int sz = int(g.sz), fz = int(g.nz), dz = int(g.dz);
   const int64_t fstride = g.f * nel;
-  for (int64_t row0 = int64_t(blockIdx.x) * RG; row0 < rows; row0 += int64_t(gridDim.x) * RG) {
-    const float* src[RG];
-    float* dst[RG];
-    bool ok[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int64_t row0 = int64_t(blockIdx.x) * rg; row0 < rows; row0 += int64_t(gridDim.x) * rg) {
+    const int nr = int(rows - row0 < rg ? rows - row0 : rg);
+    for (int p = threadIdx.x; p < nr * sz; p += blockDim.x) {
+      const int r = p / sz, oz = p - r * sz;
       const int64_t row = row0 + r;
-      ok[r] = row < rows;
-      const int64_t rr = ok[r] ? row : row0;
-      const int64_t dy = rr % g.dy;
-      const int64_t dx = (rr / g.dy) % g.dx;
-      const int64_t sf = rr / (g.dy * g.dx);
+      const int64_t dy = row % g.dy;
+      const int64_t dx = (row / g.dy) % g.dx;
+      const int64_t sf = row / (g.dy * g.dx);
       const int64_t fm = sf % g.f, s = sf / g.f;
-      const int64_t bxy = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1);
-      src[r] = frag + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz + bxy * fstride;
-      dst[r] = dense + rr * g.dz;
+      const int64_t b = s * g.alpha + frag_term(g, dx % g.sx, 0) + frag_term(g, dy % g.sy, 1) + frag_term(g, oz, 2);
+      ptab[p] = frag + b * fstride + fm * nel + ((dx / g.sx) * g.ny + dy / g.sy) * g.fpz;
     }
-    for (int dz = threadIdx.x; dz < g.dz; dz += blockDim.x) {
-      const int64_t off = ztab[dz % sz] * fstride + dz / sz;
-      float v[RG];
-#pragma unroll
-      for (int r = 0; r < RG; ++r) v[r] = ok[r] ? __ldg(src[r] + off) : 0.f;
-#pragma unroll
-      for (int r = 0; r < RG; ++r)
-        if (ok[r]) dst[r][dz] = v[r];
+    __syncthreads();
+    // one warp per fragment row: coalesced reads, scattered into dense z order
+    for (int p = warp; p < nr * sz; p += nwarps) {
+      const float* src = ptab[p];
+      float* d = buf + (p / sz) * dz + (p % sz);
+      for (int zf = lane; zf < fz; zf += 32) d[zf * sz] = __ldg(src + zf);
     }
+    __syncthreads();
+    float* dst = dense + row0 * dz;  // rows are consecutive in the dense output
+    for (int u = threadIdx.x; u < nr * dz; u += blockDim.x) dst[u] = buf[u];
+    __syncthreads();
   }
 }
 
@@ -499,8 +500,10 @@ void launch_recombine(Ctx* c, const float* frag, i64 nfrag, i64 b0, i64 f, V3 n,
   if (total == 0) return;
   KScope ks(c, VXG_K_RECOMBINE, 0.0, 8.0 * double(total));
   require(g.sz <= 256, "recombine: z stride product above 256");
+  require(g.dz <= REC_SMEM_FLOATS, "recombine: dense z extent above 8192");
+  const int rg = int(std::max<int64_t>(1, std::min<int64_t>({8, REC_SMEM_FLOATS / g.dz, REC_MAX_PAIRS / g.sz})));
   const int64_t rows = S0 * f * g.dx * g.dy;
-  recombine_kernel<<<grid_for(rows, RG, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(frag, dense, g, rows);
+  recombine_kernel<<<grid_for(rows, rg, int64_t(c->num_sms) * 8), 256, 0, c->stream>>>(frag, dense, g, rows, rg);
   c->counted();
   check_launch("recombine_kernel");
 }

@@ -255,7 +255,6 @@ struct PairCfg {
   static constexpr int THREADS = ((WORK + 31) / 32) * 32;
 };
 
-
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -298,103 +297,66 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdT
   const float* img = a.src + (s * a.f + j) * a.img_stride;
   const int tid = threadIdx.x;
 
-  // Interior box with 16-byte aligned z rows (every activation between layers:
-  // rows padded to 4 floats, tile origins multiples of vz = T - k + 1 where
-  // that is a multiple of 4): each thread loads its two z rows straight into
-  // registers and runs the z r2c there -- no staging pass through shared memory
-  const bool fused = a.dbg_fz == 0 && ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz &&
-                     (a.pz & 3) == 0 && (oz & 3) == 0 && (T & 3) == 0 &&
-                     (reinterpret_cast<uintptr_t>(img) & 15) == 0;
-  if (fused) {
-    if (tid < HP * HP) {
-      const int x = tid / HP, y = tid % HP;
-      const float4* g1 = reinterpret_cast<const float4*>(img + (int64_t(ox + x) * a.ny + oy + y) * a.pz + oz);
-      const float4* g2 = g1 + int64_t(HP) * (a.pz >> 2);  // row y + T/2
-      float2 zz[T];
-#pragma unroll
-      for (int q = 0; q < T / 4; ++q) {
-        const float4 u = __ldg(g1 + q), w = __ldg(g2 + q);
-        zz[4 * q + 0] = make_float2(u.x, w.x);
-        zz[4 * q + 1] = make_float2(u.y, w.y);
-        zz[4 * q + 2] = make_float2(u.z, w.z);
-        zz[4 * q + 3] = make_float2(u.w, w.w);
-      }
-      fft<T, false>(zz);
-      float2* s1 = sp + x * C::SX + y * C::SY;
-      float2* s2 = s1 + HP * C::SY;
-#pragma unroll
-      for (int k = 0; k < C::H; ++k) {
-        const float2 zk = zz[k];
-        const float2 zn = cconj(zz[(T - k) % T]);
-        const float2 d = csub(zk, zn);
-        s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
-        s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
-      }
-    }
-    __syncthreads();
-  } else {
   // A0: this CTA's planes (raw) -> slots (T > 32: two lane passes per z row)
-    for (int zb = 0; zb < T; zb += 32) {
-      const int lane = (tid & 31) + zb, warp = tid >> 5;
-      const int gz = oz + lane;
-      if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
-        if (lane < T) {
-          for (int x = warp; x < HP; x += NWARPS) {
-            const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.pz + gz;
-            float* d = spf + 2 * (x * C::SX) + lane;
-  #pragma unroll 8
-            for (int y = 0; y < T; ++y) {
-              cp_async4(d + 2 * C::SY * y, g, true);
-              g += a.pz;
-            }
-          }
-        }
-      } else {
-        const bool zin = lane < T && gz < a.nz;
+  for (int zb = 0; zb < T; zb += 32) {
+    const int lane = (tid & 31) + zb, warp = tid >> 5;
+    const int gz = oz + lane;
+    if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
+      if (lane < T) {
         for (int x = warp; x < HP; x += NWARPS) {
-          const int gx = ox + x;
-          const bool xin = zin && gx < a.nx;
-          const float* g = img + (int64_t(gx) * a.ny + oy) * a.pz + gz;
+          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.pz + gz;
           float* d = spf + 2 * (x * C::SX) + lane;
-  #pragma unroll 4
+#pragma unroll 8
           for (int y = 0; y < T; ++y) {
-            const bool in = xin && oy + y < a.ny;
-            if (lane < T) cp_async4(d, in ? g : img, in);
+            cp_async4(d + 2 * C::SY * y, g, true);
             g += a.pz;
-            d += 2 * C::SY;
           }
         }
       }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-  
-    // A1: z r2c, lines (x, y) and (x, y + T/2) share one complex transform
-    if (tid < HP * HP) {
-      const int x = tid / HP, y = tid % HP;
-      float2* s1 = sp + x * C::SX + y * C::SY;
-      float2* s2 = s1 + HP * C::SY;
-      float2 zz[T];
-  #pragma unroll
-      for (int q = 0; q < T / 2; ++q) {
-        const float2 r1 = s1[q], r2 = s2[q];
-        zz[2 * q] = make_float2(r1.x, r2.x);
-        zz[2 * q + 1] = make_float2(r1.y, r2.y);
-      }
-      fft<T, false>(zz);
-  #pragma unroll
-      for (int k = 0; k < C::H; ++k) {
-        const float2 zk = zz[k];
-        const float2 zn = cconj(zz[(T - k) % T]);
-        const float2 d = csub(zk, zn);
-        s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
-        s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
+    } else {
+      const bool zin = lane < T && gz < a.nz;
+      for (int x = warp; x < HP; x += NWARPS) {
+        const int gx = ox + x;
+        const bool xin = zin && gx < a.nx;
+        const float* g = img + (int64_t(gx) * a.ny + oy) * a.pz + gz;
+        float* d = spf + 2 * (x * C::SX) + lane;
+#pragma unroll 4
+        for (int y = 0; y < T; ++y) {
+          const bool in = xin && oy + y < a.ny;
+          if (lane < T) cp_async4(d, in ? g : img, in);
+          g += a.pz;
+          d += 2 * C::SY;
+        }
       }
     }
-    __syncthreads();
-  
   }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // A1: z r2c, lines (x, y) and (x, y + T/2) share one complex transform
+  if (tid < HP * HP) {
+    const int x = tid / HP, y = tid % HP;
+    float2* s1 = sp + x * C::SX + y * C::SY;
+    float2* s2 = s1 + HP * C::SY;
+    float2 zz[T];
+#pragma unroll
+    for (int q = 0; q < T / 2; ++q) {
+      const float2 r1 = s1[q], r2 = s2[q];
+      zz[2 * q] = make_float2(r1.x, r2.x);
+      zz[2 * q + 1] = make_float2(r1.y, r2.y);
+    }
+    fft<T, false>(zz);
+#pragma unroll
+    for (int k = 0; k < C::H; ++k) {
+      const float2 zk = zz[k];
+      const float2 zn = cconj(zz[(T - k) % T]);
+      const float2 d = csub(zk, zn);
+      s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
+      s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
+    }
+  }
+  __syncthreads();
 
   // B: y lines (x, kz) of this CTA's planes
   if (tid < HP * C::H) {
@@ -917,10 +879,7 @@ int64_t tile_nwp(int T, int lw) {
     default: throw invalid("tile fft: unsupported tile size");      \
   }
 
-void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a0, int64_t nblocks) {
-  static const bool no_fz = std::getenv("VXG_NO_FZ") != nullptr;
-  FwdTileArgs a = a0;
-  a.dbg_fz = no_fz ? 1 : 0;
+void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks) {
   const double nw = double(T) * T * (T / 2 + 1);
   KScope ks(c, a.kind, 0.0, double(nblocks) * (4.0 * double(T) * T * T + 8.0 * nw));
   VXG_TILE_SWITCH(fwd_t)
