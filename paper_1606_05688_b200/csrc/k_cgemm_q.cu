@@ -30,7 +30,8 @@
 //   warp 2 lane 0  W producer: one bulk copy of the item's pre-split W
 //                  (written once per layer by q_wsplit_kernel) into a 3-deep
 //                  ring shared with the TMEM A slots;
-//   warps 8-11     converters: split X into tf32 hi/lo, tcgen05.st into the
+//   warps 8-15     converters, two groups taking alternate items (a thread
+//                  per row each): split X into tf32 hi/lo, tcgen05.st into the
 //                  item's TMEM A slot (row = lane), arrive on ready[slot];
 //   warp 1         MMA issuer (one thread): 12 tcgen05.mma per item, one
 //                  commit per item (frees the A and W slot) and, after a pass's
@@ -55,7 +56,7 @@ void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uin
 namespace {
 
 using namespace tc;
-constexpr int Q_THREADS = 384;  // 12 warps
+constexpr int Q_THREADS = 512;  // 16 warps
 constexpr int Q_RAW_ROW = 144;  // 9 channel pieces of 16 B per staged row
 constexpr int Q_RAW = TC_M * Q_RAW_ROW;
 
@@ -81,7 +82,7 @@ struct QCfg {
 // ---- one-time W preparation: raw [w/16][i][j][16] complex -> per item
 // (pair p, half h, chunk kc) the matrices (w, hi/lo) x blocks (-Wi, Wr, Wi) of
 // NS x 8 tf32 in the UMMA K-major layout.
-template <int FO>
+template <int FO, bool BFC>
 __global__ void q_wsplit_kernel(const float2* __restrict__ raw, uint8_t* __restrict__ out, int64_t npairs,
                                 int f) {
   using C = QCfg<FO>;
@@ -121,7 +122,15 @@ __global__ void q_wsplit_kernel(const float2* __restrict__ raw, uint8_t* __restr
       }
       const int off = tile_off(blk * C::NS + n, kg);
       *reinterpret_cast<float4*>(item + (w * 2 + 0) * C::BMAT + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-      *reinterpret_cast<float4*>(item + (w * 2 + 1) * C::BMAT + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+      if constexpr (BFC) {
+        // bf16 correction matrix (K = 16): K 0-7 = bf16(lo), K 8-15 = bf16(hi) of the
+        // 8 channels; this thread's 4 channels are 8 bytes of each 16-byte K group
+        uint8_t* cm = item + (w * 2 + 1) * C::BMAT + tile_off(blk * C::NS + n, 0) + 8 * kg;
+        *reinterpret_cast<uint2*>(cm) = make_uint2(pack_bf16(lv[0], lv[1]), pack_bf16(lv[2], lv[3]));
+        *reinterpret_cast<uint2*>(cm + 128) = make_uint2(pack_bf16(hv[0], hv[1]), pack_bf16(hv[2], hv[3]));
+      } else {
+        *reinterpret_cast<float4*>(item + (w * 2 + 1) * C::BMAT + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+      }
     }
   }
 }
@@ -150,7 +159,11 @@ struct QArgs {
   long long* prof;
 };
 
-template <int FO>
+// BFC: 2 MMAs per product instead of 3 -- a*b ~ a_hi*b_hi (tf32) + [bf16(a_hi) |
+// bf16(a_lo)] . [bf16(b_lo) ; bf16(b_hi)] (one kind::f16 MMA, K = 16): the
+// correction terms are ~2^-11 of the product, so their bf16 rounding costs
+// ~2^-19 relative per product (3xTF32: ~2^-21).
+template <int FO, bool BFC>
 __global__ void __launch_bounds__(Q_THREADS, 1)
     cgemm_q_kernel(const __grid_constant__ CUtensorMap xmap, QArgs a) {
   using C = QCfg<FO>;
@@ -180,11 +193,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
   if (tid == 32) {
     for (int s = 0; s < C::RS; ++s) {
       mbar_init(&rfull[s], 1);    // X producer's arrive + transaction bytes
-      mbar_init(&rfree[s], 128);  // converter threads
+      mbar_init(&rfree[s], 128);  // converter threads (one group per item)
     }
     for (int s = 0; s < C::AS; ++s) {
       mbar_init(&wfull[s], 1);    // W producer's arrive + transaction bytes
-      mbar_init(&ready[s], 128);  // converter threads
+      mbar_init(&ready[s], 128);  // converter threads (one group per item)
       mbar_init(&aempty[s], 1);   // MMA commit
     }
     for (int p = 0; p < 2; ++p) {
@@ -253,18 +266,25 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     }
   } else if (warp >= 8) {
     // ---------------- converters: thread c owns row c ----------------
-    const int c = tid - 256;
+    // two converter groups, each a thread per row: warps 8-11 take the even
+    // items, warps 12-15 the odd ones, so two items' TMEM stores are in flight
+    const int c = (tid - 256) & 127;
+    const int grp = (tid - 256) >> 7;
     long long cw = 0, cb = 0;
-    int s = 0, as = 0;
+    int s = grp, as = grp;
     uint32_t ph = 0, aph = 0;
-    for (int64_t g = 0; g < nitems; ++g) {
+    for (int64_t g = grp; g < nitems; g += 2) {
       const long long t0 = a.prof ? clock64() : 0;
       mbar_wait(&rfull[s], ph);
       long long t1 = a.prof ? clock64() : 0;
       cw += t1 - t0;
       const uint8_t* raw = smem + s * Q_RAW + c * a.raw_row;
       // split X row c into tf32 hi/lo: A slot columns ((w*2 + comp)*2 + hi/lo)*8 + channel
+      // (BFC: the lo part's 8 columns hold the packed bf16 correction operand:
+      // columns 0-3 bf16(hi) of channels (0,1)..(6,7), columns 4-7 bf16(lo))
       uint32_t u[64];
+      float2 hl[4][8];
+      (void)hl;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const float4 v = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
@@ -274,8 +294,18 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
           float hi, lo;
           split_tf32(x, hi, lo);
           u[(e * 2 + 0) * 8 + ch] = __float_as_uint(hi);
-          u[(e * 2 + 1) * 8 + ch] = __float_as_uint(lo);
+          if constexpr (!BFC) u[(e * 2 + 1) * 8 + ch] = __float_as_uint(lo);
+          else hl[e][ch] = make_float2(hi, lo);
         }
+      }
+      if constexpr (BFC) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int c2 = 0; c2 < 4; ++c2) {
+            u[(e * 2 + 1) * 8 + c2] = pack_bf16(hl[e][2 * c2].x, hl[e][2 * c2 + 1].x);
+            u[(e * 2 + 1) * 8 + 4 + c2] = pack_bf16(hl[e][2 * c2].y, hl[e][2 * c2 + 1].y);
+          }
       }
       // the box may be refilled: order these generic-proxy reads before the
       // producer's next TMA (async-proxy) write into the slot
@@ -308,16 +338,19 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&ready[as]);
       if (a.prof) cb += clock64() - t1;
-      if (++s == C::RS) {
-        s = 0;
+      // both rings advance by two items per group step
+      s += 2;
+      if (s >= C::RS) {
+        s -= C::RS;
         ph ^= 1u;
       }
-      if (++as == C::AS) {
-        as = 0;
+      as += 2;
+      if (as >= C::AS) {
+        as -= C::AS;
         aph ^= 1u;
       }
     }
-    if (a.prof && c == 0) {
+    if (a.prof && c == 0 && grp == 0) {
       a.prof[blockIdx.x * 8 + 1] = cw;
       a.prof[blockIdx.x * 8 + 2] = cb;
     }
@@ -356,7 +389,22 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
           const uint64_t bm = umma_desc(wbase + (w * 2 + TERMS[k][3]) * C::BMAT + TERMS[k][2] * (NS / 8) * 256);
           mma_tf32_ta(d, am, bm, idesc, k == 0 ? acc0 : 1u);
         };
-        if (a.dbg & 16) {
+        if constexpr (BFC) {
+          // per frequency: Xr_hi [Wr|Wi]_hi, Xr_corr [Wr|Wi]_corr, Xi_hi [-Wi|Wr]_hi, Xi_corr [-Wi|Wr]_corr
+          const uint32_t idb = idesc_bf16<FO>();
+#pragma unroll
+          for (int w = 0; w < 2; ++w)
+#pragma unroll
+            for (int comp = 0; comp < 2; ++comp) {
+              const uint32_t d = tmem + uint32_t((pass * 2 + w) * FO);
+              const int blk = comp == 0 ? 1 : 0;  // B_top starts at block 1, B_bot at block 0
+              const uint32_t bb = wbase + blk * (NS / 8) * 256;
+              mma_tf32_ta(d, ta + uint32_t(((w * 2 + comp) * 2 + 0) * 8), umma_desc(bb + (w * 2 + 0) * C::BMAT), idesc,
+                          comp == 0 ? acc0 : 1u);
+              mma_bf16_ta(d, ta + uint32_t(((w * 2 + comp) * 2 + 1) * 8), umma_desc(bb + (w * 2 + 1) * C::BMAT), idb,
+                          1u);
+            }
+        } else if (a.dbg & 16) {
 #pragma unroll
           for (int k = 0; k < 6; ++k)
 #pragma unroll
@@ -367,6 +415,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 6; ++k) issue(w, k);
         }
+        (void)issue;
         umma_commit(&aempty[as]);                        // A slot and W slot reusable once these MMAs finish
         if (kc == nch - 1) umma_commit(&acc_full[pass]);  // pass accumulated
         if (++as == C::AS) {
@@ -457,13 +506,21 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
   }
 }
 
+// VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
+// tf32 + bf16-correction pair (the W layout follows the same switch)
+bool q_bf16_correction() {
+  static const bool on = std::getenv("VXG_Q_3TF32") == nullptr;
+  return on;
+}
+
 template <int FO>
 void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
   using C = QCfg<FO>;
   static_assert(C::SMEM <= 232448, "cgemm_q: shared memory");
   static PerDeviceOnce configured;
   if (configured.first()) {
-    VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_q_kernel<FO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_q_kernel<FO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    VXG_CUDA_CHECK(cudaFuncSetAttribute(cgemm_q_kernel<FO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   }
   QArgs a{};
   a.Y = g.Y;
@@ -497,7 +554,10 @@ void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
     VXG_CUDA_CHECK(cudaMemset(dprof, 0, size_t(grid) * 8 * sizeof(long long)));
     a.prof = dprof;
   }
-  cgemm_q_kernel<FO><<<grid, Q_THREADS, C::SMEM, c->stream>>>(xmap, a);
+  if (q_bf16_correction())
+    cgemm_q_kernel<FO, true><<<grid, Q_THREADS, C::SMEM, c->stream>>>(xmap, a);
+  else
+    cgemm_q_kernel<FO, false><<<grid, Q_THREADS, C::SMEM, c->stream>>>(xmap, a);
   c->counted();
   check_launch("cgemm_q_kernel");
   if (prof) {
@@ -520,8 +580,12 @@ template <int FO>
 void q_wsplit_t(Ctx* c, const float2* raw, void* out, int64_t npairs, int f) {
   using C = QCfg<FO>;
   const int64_t total = npairs * 2 * (f / TC_KC) * 2 * C::NS * 2;
-  q_wsplit_kernel<FO><<<grid_for(total, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
-      raw, static_cast<uint8_t*>(out), npairs, f);
+  if (q_bf16_correction())
+    q_wsplit_kernel<FO, true><<<grid_for(total, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
+        raw, static_cast<uint8_t*>(out), npairs, f);
+  else
+    q_wsplit_kernel<FO, false><<<grid_for(total, 256, int64_t(c->num_sms) * 16), 256, 0, c->stream>>>(
+        raw, static_cast<uint8_t*>(out), npairs, f);
   c->counted();
   check_launch("q_wsplit_kernel");
 }

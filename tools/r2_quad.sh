@@ -1,28 +1,7 @@
 mkdir -p gpurun_out
-TAG=${TAG:-slow1}
-cat > /tmp/loop.py <<'PY'
-import sys, os, time
-sys.path.insert(0, '.')
-import torch, paper_1606_05688_b200 as v
-ctx = v.Context(0)
-g = torch.Generator(device="cuda").manual_seed(1)
-n, S = 85, 64
-x = torch.rand((S, 80, n, n, n), device="cuda", generator=g) * 2 - 1
-w = (torch.rand((80, 80, 5, 5, 5), device="cuda", generator=g) * 2 - 1) * 0.02
-b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
-p = v.ConvLayerParams(w, b, "relu")
-T = int(os.environ.get("T", "24"))
-for i in range(6):
-    ctx.profile(True)
-    t0 = time.perf_counter()
-    y = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
-    ctx.sync()
-    ks = ctx.kernel_stats()
-    ctx.profile(False)
-    print(i, "wall %.1f ms" % ((time.perf_counter() - t0) * 1e3), {k: round(s["seconds"] * 1e3, 2) for k, s in ks.items()}, flush=True)
-    del y
-PY
-VXG_TC_PROF=1 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_quad24.txt 2>&1
-VXG_TC_PAIR=1 VXG_TC_PROF=1 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_pair24.txt 2>&1
-VXG_TC_PROF=1 T=32 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_quad32.txt 2>&1
-nvidia-smi --query-gpu=clocks.sm,clocks.mem,power.draw,clocks_event_reasons.active --format=csv >> gpurun_out/${TAG}_smi.txt
+TAG=${TAG:-bf3}
+timeout 900 python -m pytest tests/test_gpu_primitives.py -q -x -k "tensor_core or every_tile or pair_tile or match_ffma or conv_matches or fused" > gpurun_out/${TAG}_pytest.txt 2>&1
+for T in 32 24; do
+  VXG_TC_PROF=1 VXG_FFT_TILE=$T timeout 300 python tools/kbench.py --which conv --S 64 --n 85 > gpurun_out/${TAG}_T$T.txt 2>&1
+  VXG_Q_3TF32=1 VXG_TC_PROF=1 VXG_FFT_TILE=$T timeout 300 python tools/kbench.py --which conv --S 64 --n 85 > gpurun_out/${TAG}_3tf_T$T.txt 2>&1
+done
