@@ -32,9 +32,12 @@ NET = "n537"
 # smallest admissible cubic patch per bundled net: the CPU
 # reference runs there
 SMALLEST = {"n337": 92, "n537": 170, "n726": 120, "n926": 158}
-# ncu DRAM bytes per launch / the launch's algorithmic bytes (profiles/r1_ncu_summary.md):
-# cgemm_tc (M = 1728 rows, T = 32, final capture r1e): (21.89 + 19.82) GB / (2 x 19.26 GB X, Y + 1.78 GB W)
-TRAFFIC_RATIO = {"cgemm": round((21.89 + 19.82) / (2 * 19.26 + 1.78), 3)}
+# ncu dram__bytes_read.sum + dram__bytes_write.sum / algorithmic bytes of one
+# cgemm_q_kernel<80> launch (kbench 80 -> 80 k5, S = 64, n = 85, T = 32, 1728 rows:
+# 27.45 + 19.23 GB against 8 * 17408 * (2 * 1728 * 80 + 80 * 80) B = 39.39 GB),
+# profiles/r2/r2g_layer_full.txt
+TRAFFIC_RATIO = {"cgemm": round((27.445 + 19.230) / 39.394, 3)}
+TRAFFIC_SOURCE = "profiles/r2/r2g_layer_full.txt"
 FFMA_FALLBACK_TFLOPS = 74.4  # 148 SM x 128 x 2 x 1.965 GHz (nominal), used only if measurement fails
 
 
@@ -529,15 +532,18 @@ def main():
     tc_used = os.environ.get("VXG_NO_TC", "0") in ("", "0")
     ds = kstats[dom]
     if ds["flops"] > 0 and dom == "cgemm" and tc_used:
-        # tcgen05 kind::tf32 with a 3xTF32 split: 3 tensor MMAs per real product,
-        # so the algorithmic-fp32 ceiling is the tf32 peak (1/2 of the measured
-        # dense bf16 peak) / 3.  The contraction also moves X + Y + W through HBM:
-        # report against whichever bound is slower for its per-launch work.
+        # tcgen05: a tf32 MMA for a_hi*b_hi plus one kind::f16 MMA (K = 16, same
+        # time as a K = 8 tf32 MMA) for both bf16 correction terms -- 2 tf32-MMA
+        # equivalents per real product (VXG_Q_3TF32=1: the 3xTF32 split, 3) -- so
+        # the algorithmic-fp32 ceiling is the tf32 peak (1/2 of the measured dense
+        # bf16 peak) / 2 (or / 3).  The contraction also moves X + Y + W through
+        # HBM: report against whichever bound is slower for its per-launch work.
         tflops = ds["flops"] / ds["seconds"] / 1e12
         gbps = ds["bytes"] / ds["seconds"] / 1e9
         # sustained figure: the contraction runs inside a seconds-long step
         tkey = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
-        tpeak = peaks.get(tkey, 1395.3) / 2.0 / 3.0
+        split = 3.0 if os.environ.get("VXG_Q_3TF32") else 2.0
+        tpeak = peaks.get(tkey, 1395.3) / 2.0 / split
         t_tensor = ds["flops"] / (tpeak * 1e12)
         t_hbm = ds["bytes"] / (peaks["hbm_gbs"] * 1e9)
         if t_hbm >= t_tensor:
@@ -547,7 +553,7 @@ def main():
         else:
             roof = {"kernel": dom, "bound": "tensor", "achieved": tflops, "peak": tpeak,
                     "unit": "TFLOP/s", "frac": tflops / tpeak,
-                    "peak_source": f"MEASURED_PEAKS.json {tkey} ({peaks_src}) / 2 (tf32) / 3 (3xTF32 split)",
+                    "peak_source": f"MEASURED_PEAKS.json {tkey} ({peaks_src}) / 2 (tf32) / {split:g} (MMAs per product)",
                     "hbm_frac": gbps / peaks["hbm_gbs"]}
         roof["tensor_peak_tflops"] = tpeak
         roof["vs_fp32_ffma_peak"] = tflops / ffma_peak
@@ -562,11 +568,11 @@ def main():
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src}
     # DRAM traffic / algorithmic bytes of the dominant kernel from the committed
-    # ncu --set full capture (profiles/r1_ncu_summary.md), applied per launch
+    # ncu --set full capture (TRAFFIC_SOURCE), applied per launch
     ratio = TRAFFIC_RATIO.get(dom)
     roof["traffic"] = ratio * ds["bytes"] / ds["launches"] if ratio else None
     roof["traffic_source"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum / algorithmic bytes = "
-                              f"{ratio} (profiles/r1_ncu_summary.md)") if ratio else None
+                              f"{ratio} ({TRAFFIC_SOURCE})") if ratio else None
     roof["per_launch"] = {"flops": ds["flops"] / ds["launches"], "bytes": ds["bytes"] / ds["launches"],
                           "seconds": ds["seconds"] / ds["launches"]}
     roof_l = []
