@@ -57,7 +57,6 @@ namespace {
 
 using namespace tc;
 constexpr int Q_THREADS = 512;  // 16 warps
-constexpr int QG = 8;           // row blocks per tile-order group
 constexpr int Q_RAW_ROW = 144;  // 9 channel pieces of 16 B per staged row
 constexpr int Q_RAW = TC_M * Q_RAW_ROW;
 
@@ -212,28 +211,16 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = *tmem_slot;
 
-  // tile t (local) -> (line block wb, row block, quad q, half h), (q, h)
-  // fastest; row blocks in groups of QG: concurrent CTAs cover ~148/(8 QG)
-  // line blocks at once, so a W item is shared by at most QG CTAs at a time
-  // (with every row block of one line block in flight, 148 CTAs hammered the
-  // same few MB of W and large launches ran at half speed)
-  const int64_t full = a.mblocks / QG;              // complete groups
-  const int last = int(a.mblocks - full * QG);      // rows blocks in the partial group
+  // tile t (local) -> (line block wb, row block, quad q, half h), (q, h) fastest
+  // (grouping row blocks so fewer CTAs share a W item at a time made no
+  // difference, profiles/r2_experiments.md §7)
   auto tile_of = [&](int64_t lt, int64_t& wb, int64_t& m0, int& q, int& h) {
     const int64_t t = blockIdx.x + lt * gridDim.x;
     h = int(t & 1);
     q = int((t >> 1) & 3);
     const int64_t rest = t >> 3;
-    const int64_t span = a.nwb * QG;
-    if (rest < full * span) {
-      const int64_t gi = rest / span, r2 = rest - gi * span;
-      wb = r2 / QG;
-      m0 = (gi * QG + (r2 - wb * QG)) * TC_M;
-    } else {
-      const int64_t r3 = rest - full * span;
-      wb = r3 / last;
-      m0 = (full * QG + (r3 - wb * last)) * TC_M;
-    }
+    m0 = (rest % a.mblocks) * TC_M;
+    wb = rest / a.mblocks;
   };
 
   if (warp == 0 || warp == 2) {
