@@ -166,6 +166,20 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
   int64_t rows = std::max<int64_t>(1, avail / per_row);
   rows = std::min(rows, M);
   rows = std::min<int64_t>(rows, ((int64_t(1) << 31) - 1) / std::max(f, fo));
+  // Chunks of at most ~2048 rows: launches over 8000 rows (38 GB spectrum
+  // buffers at T = 24) alternated between full speed and half speed in the
+  // contraction from one identical launch to the next, while the same rows in
+  // four chunks ran at full speed every time (profiles/r2_experiments.md §8);
+  // the extra kernel-spectrum reads cost ~2 %.  VXG_MAX_ROWS overrides (0: none).
+  static const int64_t max_rows = [] {
+    const char* e = std::getenv("VXG_MAX_ROWS");
+    return e ? int64_t(std::atoll(e)) : int64_t(2048);
+  }();
+  if (max_rows > 0 && rows > max_rows) rows = max_rows;
+  {
+    const int64_t nchunks = (M + rows - 1) / rows;
+    rows = (M + nchunks - 1) / nchunks;  // balanced chunks
+  }
   if (trace_on())
     std::fprintf(stderr, "[vxg] conv_fft S=%lld f=%lld fo=%lld n=%lld T=%d tiles=%lld M=%lld rows=%lld tc=%d\n",
                  (long long)S, (long long)f, (long long)fo, (long long)n.x, T, (long long)plan.tiles,

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-TAG=${TAG:-slow2}
+TAG=${TAG:-slow3}
 cat > /tmp/loop.py <<'PY'
 import sys, os, time
 sys.path.insert(0, '.')
@@ -18,8 +18,10 @@ for i in range(6):
     ctx.sync()
     ks = ctx.kernel_stats()
     ctx.profile(False)
-    print(i, {k: round(s["seconds"] * 1e3, 2) for k, s in ks.items()}, flush=True)
+    print(i, {k: (s["launches"], round(s["seconds"] * 1e3, 2)) for k, s in ks.items()}, flush=True)
     del y
 PY
-VXG_TC_PROF=1 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_quad24.txt 2>&1
-VXG_TC_PROF=1 T=32 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_quad32.txt 2>&1
+T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_full.txt 2>&1
+VXG_MAX_ROWS=2000 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_cap2000.txt 2>&1
+VXG_MAX_ROWS=1024 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_cap1024.txt 2>&1
+VXG_TC_PAIR=1 T=24 timeout 300 python /tmp/loop.py > gpurun_out/${TAG}_pair.txt 2>&1
