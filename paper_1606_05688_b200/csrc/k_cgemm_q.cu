@@ -1,8 +1,13 @@
 // K3 on the 5th-generation tensor cores, quad-frequency tiles: the
 // per-frequency complex contraction Y[w](m, i) = sum_j X[w](m, j) W[w](i, j)
-// (the MAC of proj/include/voxin/layers.hpp:245-251, 330-344) as tcgen05.mma
-// kind::tf32 with a 3xTF32 split (a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi,
-// fp32 accumulation in TMEM).
+// (the MAC of proj/include/voxin/layers.hpp:245-251, 330-344) on tcgen05.mma
+// with fp32 accumulation in TMEM.  Each real product costs two MMAs: a
+// kind::tf32 MMA for a_hi*b_hi and one kind::f16 MMA (K = 16) for both
+// correction terms, [bf16(a_hi) | bf16(a_lo)] . [bf16(b_lo) ; bf16(b_hi)]
+// (a_hi = a with 13 mantissa bits cleared, a_lo = a - a_hi).  The correction
+// terms are ~2^-11 of the product, so their bf16 rounding adds ~2^-19 relative
+// error per product; VXG_Q_3TF32=1 selects the 3xTF32 split instead
+// (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi, three tf32 MMAs).
 //
 // Why quads: spectra are line-major ([w/16][row][map][16 w], 128-byte lines,
 // the layout the tile transforms read and write whole).  A store that fills a
@@ -11,8 +16,8 @@
 // 32-byte sector of every line it writes) x 128 rows x half of the output maps
 // (NS = fo / 2), and each MMA is the real-block product
 //   [Dr | Di] += Xr [Wr | Wi] + Xi [-Wi | Wr]        (N = 2 NS = fo columns)
-// with W stored once per hi/lo part as three N-blocks (-Wi, Wr, Wi): the B
-// operand [-Wi | Wr] starts at block 0 and [Wr | Wi] at block 1.
+// with W stored once per part (hi; correction) as three N-blocks (-Wi, Wr, Wi):
+// the B operand [-Wi | Wr] starts at block 0 and [Wr | Wi] at block 1.
 //
 // TMEM: four accumulators (one per frequency, fo columns each, <= 320) + three
 // 64-column A slots.  The K loop of a tile runs in two passes (frequencies 0-1
@@ -33,7 +38,8 @@
 //   warps 8-15     converters, two groups taking alternate items (a thread
 //                  per row each): split X into tf32 hi/lo, tcgen05.st into the
 //                  item's TMEM A slot (row = lane), arrive on ready[slot];
-//   warp 1         MMA issuer (one thread): 12 tcgen05.mma per item, one
+//   warp 1         MMA issuer (one thread): 8 tcgen05.mma per item (12 with
+//                  the 3xTF32 split), one
 //                  commit per item (frees the A and W slot) and, after a pass's
 //                  last chunk, acc_full[pass];
 //   warps 4-7      epilogue (TMEM lane quadrants 0-3).
@@ -155,7 +161,8 @@ struct QArgs {
   int64_t nwb;
   int raw_row;      // staged row stride (16 B x box channels)
   int raw_bytes;    // bytes one X box lands in shared memory
-  int dbg;          // VXG_TC_DBG experiment switches (results invalid when set)
+  int dbg;          // VXG_TC_DBG experiment switches, results invalid when set:
+                    // 2 skip the Y stores, 4 skip the epilogue's TMEM loads, 8 skip the A stores
   long long* prof;
 };
 
@@ -385,8 +392,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         constexpr int TERMS[6][4] = {{0, 0, 1, 0}, {0, 1, 1, 0}, {0, 0, 1, 1},
                                      {1, 0, 0, 1}, {1, 0, 0, 0}, {1, 1, 0, 0}};
         auto issue = [&](int w, int k) {
-          const int acc = (a.dbg & 1) ? ((pass * 2 + w + 2 * (k & 1)) & 3) : pass * 2 + w;
-          const uint32_t d = tmem + uint32_t(acc * FO);
+          const uint32_t d = tmem + uint32_t((pass * 2 + w) * FO);
           const uint32_t am = ta + uint32_t(((w * 2 + TERMS[k][0]) * 2 + TERMS[k][1]) * 8);
           const uint64_t bm = umma_desc(wbase + (w * 2 + TERMS[k][3]) * C::BMAT + TERMS[k][2] * (NS / 8) * 256);
           mma_tf32_ta(d, am, bm, idesc, k == 0 ? acc0 : 1u);
@@ -406,11 +412,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
               mma_bf16_ta(d, ta + uint32_t(((w * 2 + comp) * 2 + 1) * 8), umma_desc(bb + (w * 2 + 1) * C::BMAT), idb,
                           1u);
             }
-        } else if (a.dbg & 16) {
-#pragma unroll
-          for (int k = 0; k < 6; ++k)
-#pragma unroll
-            for (int w = 0; w < 2; ++w) issue(w, k);
         } else {
 #pragma unroll
           for (int w = 0; w < 2; ++w)
