@@ -208,11 +208,15 @@ struct Ctx {
   void counted(i64 n = 1) { launches += n; }
   // give the held arena block back to the pool (not while a forward uses it)
   bool drop_held() {
-    if (!held || held_busy) return false;
-    cudaFreeAsync(held, stream);
-    held = nullptr;
-    held_bytes = 0;
-    held_bytes = 0;
+    void* p = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);  // another context's thread may call this (release_idle_memory)
+      if (!held || held_busy) return false;
+      p = held;
+      held = nullptr;
+      held_bytes = 0;
+    }
+    cudaFreeAsync(p, stream);
     return true;
   }
 };

@@ -538,23 +538,38 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
       std::fprintf(stderr, "[vxg] forward arena: need %lld held %lld avail %lld (budget left %lld, device %lld)\n",
                    (long long)arena_bytes, (long long)held, (long long)avail0, (long long)c->avail(),
                    (long long)c->device_free());
-    if (held >= arena_bytes && held <= avail0) {
-      arena_bytes = held;
-      c->charge(arena_bytes);
+    bool reuse = false;
+    {
+      std::lock_guard<std::mutex> lk(c->mu);  // release_idle_memory may drop an idle block
+      if (c->held && c->held_bytes >= arena_bytes && c->held_bytes <= avail0) {
+        reuse = true;
+        arena_bytes = c->held_bytes;
+        c->held_busy = true;
+      }
+    }
+    if (reuse) {
+      try {
+        c->charge(arena_bytes);
+      } catch (...) {
+        c->held_busy = false;
+        throw;
+      }
     } else {
       c->drop_held();
       DevBuf blk(c, arena_bytes);  // charged
+      std::lock_guard<std::mutex> lk(c->mu);
       c->held = blk.release_ptr();
       c->held_bytes = arena_bytes;
+      c->held_busy = true;
     }
     struct Busy {
       Ctx* c;
       ~Busy() {
-        c->held_busy = false;
         c->release(c->held_bytes);  // idle: kept, not charged
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->held_busy = false;
       }
     } busy{c};
-    c->held_busy = true;
     Arena arena;
     arena.reset(c->held, arena_bytes);
     struct Scope {
