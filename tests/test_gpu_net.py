@@ -329,3 +329,26 @@ def test_run_bench_csv_matches_the_reference_columns(tmp_path):
         e, model, audited, vps, sec = int(r[0]), float(r[1]), float(r[2]), float(r[3]), float(r[4])
         assert vps > 0 and sec > 0 and model > 0 and 0.5 * model <= audited <= budget / 4
         assert abs(sum(float(x) for x in r[5:]) * 1e-3 - sec) <= 0.25 * sec
+
+
+def test_held_arena_yields_to_other_contexts():
+    """The forward's arena block stays with its context between forwards (no
+    pool remap per forward) but is not charged while idle, and yields to a new
+    context's budget and to Context.trim() (vxg_ctx_trim)."""
+    import torch
+    import paper_1606_05688_b200 as v
+    from paper_1606_05688_b200.bundled_nets import NETS
+    net = v.parse_network_spec(NETS["n337"])
+    a = v.Context(0)
+    m = v.Model(net, v.random_weights(net, 1), a)
+    x = torch.from_numpy(v.fill_random((1, 1, 148, 148, 148), 3)).cuda()
+    y1, _ = m.forward(x)
+    assert a.memory()["current"] < 4 * 2 ** 30  # weights and spectra only: the idle block is not charged
+    y2, _ = m.forward(x)                         # reuses the held block
+    assert torch.equal(y1, y2)
+    b = v.Context(0)                             # creation hands idle caches back first
+    assert b.memory()["budget"] > 100 * 2 ** 30
+    a.trim()
+    y3, _ = m.forward(x)
+    assert torch.equal(y1, y3)
+    m.close()
