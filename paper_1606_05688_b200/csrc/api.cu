@@ -847,8 +847,10 @@ int vxg_model_forward_many(vxg_model* model, int64_t count, const float* const* 
       const int b = int(k % nbuf);
       if (nbuf == 2 && k + 1 < count) h2d(k + 1);  // prefetch under this forward
       VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, h2d_done[b], 0));
-      if (k >= nbuf) VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, d2h_done[b], 0));
-      m.forward(p, din[b].as<float>(), dout[b].as<float>(), cache_spectra != 0, nullptr);
+      // the download of the patch that used this output buffer only has to end
+      // before this forward writes its dense output: it runs under the forward
+      m.forward(p, din[b].as<float>(), dout[b].as<float>(), cache_spectra != 0, nullptr,
+                k >= nbuf ? d2h_done[b] : nullptr);
       VXG_CUDA_CHECK(cudaEventRecord(fwd_done[b], c->stream));
       VXG_CUDA_CHECK(cudaStreamWaitEvent(st.out, fwd_done[b], 0));
       VXG_CUDA_CHECK(cudaMemcpyAsync(outputs[k], dout[b].get(), size_t(nout) * 4, cudaMemcpyDeviceToHost,

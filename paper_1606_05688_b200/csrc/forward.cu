@@ -487,7 +487,7 @@ int64_t Model::plan_bytes(const ForwardPlan& p, bool cache, int64_t target_rows)
 }
 
 void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache,
-                    std::vector<double>* layer_seconds) {
+                    std::vector<double>* layer_seconds, cudaEvent_t before_output) {
   require(has_weights, "execute: planning-only model has no weights");
   EventTimer timer(c->stream, layer_seconds != nullptr);
   auto all_spectra = [&] {
@@ -592,6 +592,7 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
     if (!cache) spectra.clear();  // back to the arena (stream-ordered reuse only)
     const size_t nwin = p.windows.size() / 3;
     const Shape& fin = p.shapes.back();
+    if (before_output) VXG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, before_output, 0));
     if (nwin == 0) {
       VXG_CUDA_CHECK(cudaMemcpy2DAsync(d_dense, size_t(fin.n.z) * 4, frags.get(), size_t(p.pz.back()) * 4,
                                        size_t(fin.n.z) * 4, size_t(p.S * fin.f * fin.n.x * fin.n.y),

@@ -70,8 +70,11 @@ struct Model {
   int64_t plan_bytes(const ForwardPlan& p, bool cache_spectra, int64_t target_rows = 0) const;
   // runs the forward on a device input; writes the dense output (device);
   // layer_seconds (optional) gets per-layer device time
+  // before_output (optional): an event the stream waits on just before the
+  // dense output is written (the streaming API lets the previous patch's
+  // download from the same buffer run under this forward)
   void forward(const ForwardPlan& p, const float* d_in, float* d_dense, bool cache_spectra,
-               std::vector<double>* layer_seconds);
+               std::vector<double>* layer_seconds, cudaEvent_t before_output = nullptr);
   const float2* spectra_for(int ci, const FftPlan& plan, bool cache);
   // Measured-time planning: times every admissible tile size (and the direct
   // kernel where the model gives it a chance) on sample inputs of each conv
