@@ -91,7 +91,10 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     const double flops = 8.0 * M * double(f) * double(fo) * nw;
     const double cta = 140e-9 * std::pow(double(T) / 32.0, 3.0) * std::log2(double(T)) / 5.0;
     const double bytes = 16.0 * M * double(f + fo) * nw;
-    p.cost = flops / (tc ? 150e12 : 40e12) + M * double(f + fo) * cta + bytes / 5e12;
+    // T = 36 / 40 run on CTA pairs at one pair per SM: measured ~1.5x the
+    // per-(tile, channel) time the T^3 log T scaling predicts
+    const double big = T >= 36 ? 1.5 : 1.0;
+    p.cost = flops / (tc ? 150e12 : 40e12) + M * double(f + fo) * cta * big + bytes / 5e12;
     if (p.cost < best.cost) best = p;
   }
   if (best.T == 0) throw invalid("conv fft: no supported tile size covers the kernel");
