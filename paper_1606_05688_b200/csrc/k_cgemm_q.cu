@@ -512,8 +512,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
 // VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
 // tf32 + bf16-correction pair (the W layout follows the same switch)
 bool q_bf16_correction() {
-  static const bool on = std::getenv("VXG_Q_3TF32") == nullptr;
-  return on;
+  const char* e = std::getenv("VXG_Q_3TF32");
+  return !(e && std::strcmp(e, "0") != 0);
 }
 
 template <int FO>

@@ -433,3 +433,20 @@ def test_conv_fft_fused_z_load_vs_oracle(oracle, ctx, T):
     got = v.conv_fft_tiled(_cuda(x), v.ConvLayerParams(_cuda(w), _cuda(b), "relu"), T, tensor_cores=True,
                            cta_pair=True, ctx=ctx)
     assert rel_error(got.cpu().numpy(), oracle.conv(x, w, b, True)) <= 1e-4
+
+
+@pytest.mark.parametrize("fo", [32, 80])
+def test_conv_fft_quad_tiles_3xtf32_split(oracle, ctx, monkeypatch, fo):
+    """The quad-tile contraction with the 3xTF32 split (VXG_Q_3TF32=1: three tf32
+    MMAs per product instead of tf32 + one bf16 correction MMA; the W layout
+    follows the same switch) against the C oracle."""
+    import paper_1606_05688_b200 as v
+    monkeypatch.setenv("VXG_Q_3TF32", "1")
+    S, f, k, T = 2, 16, (3, 3, 3), 16
+    n = (T + 9, 2 * T - 1, T + 4)
+    rng = np.random.default_rng(fo + 7)
+    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 27))).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+    got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=True, ctx=ctx)
+    assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
