@@ -82,6 +82,9 @@ void tc_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, 
 // quad-frequency tiles (k_cgemm_q.cu, the default tensor-core contraction):
 // sector-complete epilogue stores, pass-split accumulators
 bool tc_quad_enabled();
+// quad tiles: tf32 + bf16-correction MMAs (default) or the 3xTF32 split
+// (VXG_Q_3TF32=1); the pre-split W layout follows the same switch
+bool q_bf16_correction();
 int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
 void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
 void launch_cgemm_q(Ctx* c, const GemmArgs& a, int64_t npairs);

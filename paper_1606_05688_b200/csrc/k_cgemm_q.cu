@@ -59,6 +59,13 @@ namespace vxg {
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                            const uint64_t* strides, const uint32_t* box);
 
+// VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
+// tf32 + bf16-correction pair (the W layout follows the same switch)
+bool q_bf16_correction() {
+  const char* e = std::getenv("VXG_Q_3TF32");
+  return !(e && std::strcmp(e, "0") != 0);
+}
+
 namespace {
 
 using namespace tc;
@@ -509,12 +516,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
   }
 }
 
-// VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
-// tf32 + bf16-correction pair (the W layout follows the same switch)
-bool q_bf16_correction() {
-  const char* e = std::getenv("VXG_Q_3TF32");
-  return !(e && std::strcmp(e, "0") != 0);
-}
 
 template <int FO>
 void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
