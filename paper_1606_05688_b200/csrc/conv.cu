@@ -23,6 +23,12 @@ bool ypair_enabled() {
   return e && std::strcmp(e, "1") == 0;
 }
 
+// VXG_NO_FUSED_F1=1: single-input-map layers go through Y like the others
+bool fused_f1_enabled() {
+  const char* e = std::getenv("VXG_NO_FUSED_F1");
+  return !(e && std::strcmp(e, "0") != 0);
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("VXG_NO_TC");
   return e && std::strcmp(e, "0") != 0;
@@ -48,7 +54,7 @@ int64_t fft_reserved_rows() {
 }
 
 int64_t fft_chunk_bytes(const FftPlan& plan, int64_t f, int64_t fo, int64_t rows) {
-  return rows * (f + fo) * plan.nwp * 8;
+  return rows * (plan.fused_f1 ? f : f + fo) * plan.nwp * 8;
 }
 
 FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
@@ -82,6 +88,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 36;
     p.ylw = (tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
     p.nwp = tile_nwp(T, p.lw);
+    p.fused_f1 = f == 1 && p.inv_pair && !p.tc && fused_f1_enabled();
     const double M = double(S) * double(p.tiles);
     const double nw = double(T) * T * (T / 2 + 1);
     // Modelled seconds (calibrated on B200 with tools/kbench.py): the
@@ -111,6 +118,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   p.lw = 16;
   p.ylw = (p.tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
   p.nwp = tile_nwp(T, p.lw);
+  p.fused_f1 = f == 1 && p.inv_pair && !p.tc && fused_f1_enabled();
   return p;
 }
 
@@ -189,7 +197,7 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
                  (long long)M, (long long)rows, int(plan.tc));
   DevBuf X(c, rows * f * plan.nwp * 8);
   DevBuf Ybuf;
-  Ybuf.alloc(c, rows * fo * plan.nwp * 8);
+  if (!plan.fused_f1) Ybuf.alloc(c, rows * fo * plan.nwp * 8);
   const DevBuf& Y = Ybuf;
 
   for (int64_t m0 = 0; m0 < M; m0 += rows) {
@@ -222,10 +230,13 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
     ga.T = T;
     ga.ypair = plan.ylw == 2 ? 1 : 0;
     ga.quad = plan.quad ? 1 : 0;
-    if (plan.tc)
+    if (plan.fused_f1) {
+      // the contraction is elementwise (one input map): done in the inverse's loads
+    } else if (plan.tc) {
       launch_cgemm_tc(c, ga, plan.nwp / 2);
-    else
+    } else {
       launch_cgemm(c, ga, plan.nwp / 16);
+    }
 
     InvTileArgs ia{};
     ia.spec = Y.as<float2>();
@@ -245,6 +256,11 @@ int64_t conv_fft_device(Ctx* c, const float* in, int64_t S, int64_t f, V3 n, con
     ia.lw = plan.ylw;
     ia.nwp = plan.nwp;
     ia.pair = plan.inv_pair;
+    if (plan.fused_f1) {
+      ia.spec = X.as<float2>();
+      ia.wsp = wspec;
+      ia.w_fo = fo;
+    }
     launch_tile_inv(c, T, ia, mc * fo);
   }
   return rows;

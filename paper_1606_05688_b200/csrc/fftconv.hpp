@@ -44,6 +44,11 @@ struct InvTileArgs {
   int lw = 16;
   bool pair = false;         // CTA-pair transform (tile_inv_pair_kernel)
   int64_t nwp = 0;           // frequencies per (row, map) in the spectrum buffer
+  // single input map (f = 1) fused with the contraction: spec holds the input
+  // spectra X ([w/16][mstride][1][16]) and the inverse multiplies each line by
+  // the kernel spectrum of its output map (wsp, [w/16][w_fo][1][16]) on load
+  const float2* wsp = nullptr;
+  int64_t w_fo = 0;
 };
 
 struct GemmArgs {
@@ -104,6 +109,7 @@ struct FftPlan {
                      // 2 frequencies x all maps (k_cgemm_tc.cu); the measured planner picks
   bool pair = false;     // forward tile transform on a CTA pair (T >= 24)
   bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
+  bool fused_f1 = false; // f = 1, FFMA: the elementwise contraction happens in the inverse's loads (no Y)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };

@@ -629,7 +629,17 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
     const float2* src = a.spec + (ml * a.fo + i) * lw;
     const int64_t wb_stride = a.mstride * a.fo * lw;
     const int t0 = x0 * C::H + tid;  // ky * H + kz, ky = x0 + tid / H
-    if (tma) {
+    if (a.wsp) {
+      // f = 1: Y[w](row, i) = X[w](row) W[w](i), formed on load (lw = 16)
+      const float2* sx = a.spec + ml * 16;
+      const float2* sw = a.wsp + i * 16;
+      const int64_t xs = a.mstride * 16, ws = a.w_fo * 16;
+#pragma unroll
+      for (int kx = 0; kx < T; ++kx) {
+        const int w = kx * T * C::H + t0;
+        v[kx] = cmul(__ldg(sx + int64_t(w >> 4) * xs + (w & 15)), __ldg(sw + int64_t(w >> 4) * ws + (w & 15)));
+      }
+    } else if (tma) {
     } else if ((T * C::H) % 16 == 0 && lw == 16) {
       const float2* g = src + int64_t(t0 >> 4) * wb_stride + (t0 & 15);
       const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
