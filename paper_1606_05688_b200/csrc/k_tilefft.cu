@@ -459,7 +459,7 @@ struct Pair2Cfg {
 };
 
 template <int T>
-__global__ void __launch_bounds__(Pair2Cfg<T>::THREADS, 2) tile_fwd_pair2_kernel(FwdTileArgs a) {
+__global__ void __launch_bounds__(Pair2Cfg<T>::THREADS) tile_fwd_pair2_kernel(FwdTileArgs a) {
   using C = TileCfg<T>;
   using P = PairCfg<T>;
   constexpr int HP = P::HP;
@@ -937,159 +937,6 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_inv_pair_kernel(InvT
   }
 }
 
-// ---- K4 on a CTA pair, two threads per line (see tile_fwd_pair2_kernel) ----------
-template <int T>
-__global__ void __launch_bounds__(Pair2Cfg<T>::THREADS, 2) tile_inv_pair2_kernel(InvTileArgs a) {
-  using C = TileCfg<T>;
-  using P = PairCfg<T>;
-  constexpr int HP = P::HP;
-  constexpr int M = T / 2;
-  constexpr int THREADS = Pair2Cfg<T>::THREADS;
-  constexpr int NWARPS = THREADS / 32;
-  constexpr int LINES = THREADS / 2;
-  extern __shared__ float2 sp[];
-  float* spf = reinterpret_cast<float*>(sp);
-  const unsigned r = cluster_rank();
-  const int64_t blk = blockIdx.x >> 1;
-  const int64_t i = blk % a.fo;
-  const int64_t ml = blk / a.fo;
-  const int64_t m = a.m0 + ml;
-  const int64_t s = m / a.tiles_per_img;
-  const int64_t t = m % a.tiles_per_img;
-  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
-  const int tid = threadIdx.x;
-  const int half = tid & 1, line = tid >> 1;
-  const int x0 = int(r) * HP;  // my planes [x0, x0 + HP)
-
-  // A+B: x lines (ky in my half, all kz) from HBM: lane h loads kx in
-  // [h M, (h+1) M), ends with x = 2q + h and writes it to the plane's owner
-  {
-    const bool live = line < HP * C::H;
-    const int t0 = x0 * C::H + (live ? line : 0);  // ky * H + kz
-    float2 v[M];
-    if (a.wsp) {
-      const float2* sx = a.spec + ml * 16;
-      const float2* sw = a.wsp + i * 16;
-      const int64_t xs = a.mstride * 16, ws = a.w_fo * 16;
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        const int w = (half * M + q) * T * C::H + t0;
-        v[q] = live ? cmul(__ldg(sx + int64_t(w >> 4) * xs + (w & 15)), __ldg(sw + int64_t(w >> 4) * ws + (w & 15)))
-                    : make_float2(0.f, 0.f);
-      }
-    } else {
-      const float2* src = a.spec + (ml * a.fo + i) * 16;
-      const int64_t wb_stride = a.mstride * a.fo * 16;
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        const int w = (half * M + q) * T * C::H + t0;
-        v[q] = live ? __ldg(src + int64_t(w >> 4) * wb_stride + (w & 15)) : make_float2(0.f, 0.f);
-      }
-    }
-    fft_split2<T, true>(v, half);
-    if (live) {
-      const int ky = x0 + line / C::H, kz = line % C::H;
-      float2* base = sp + ky * C::SY + kz;
-      const uint32_t pbase = peer_addr(base, r ^ 1u);
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        // plane x = 2q + h lives in CTA 0 for q < M/2, at local plane x mod HP
-        const int xl = (2 * q + half) % HP;
-        if ((q < M / 2) == (r == 0)) base[xl * C::SX] = v[q];
-        else st_peer(pbase + uint32_t(xl * C::SX * 8), v[q]);
-      }
-    }
-  }
-  cluster_arrive();
-  cluster_wait();
-
-  // crop planes owned here
-  const int xa = max(a.cx, x0), xb = min(a.cx + a.vx, x0 + HP);
-  const int nxl = max(0, xb - xa);
-
-  // C: y lines for my crop planes
-  for (int l0 = 0; l0 < nxl * C::H; l0 += LINES) {
-    const int l = l0 + line;
-    const bool live = l < nxl * C::H;
-    const int kz = live ? l % C::H : 0, xl = xa - x0 + (live ? l / C::H : 0);
-    float2* base = sp + xl * C::SX + kz;
-    float2 v[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) v[q] = live ? base[(half * M + q) * C::SY] : make_float2(0.f, 0.f);
-    fft_split2<T, true>(v, half);
-    __syncwarp();  // the lane pair has read its line before writing it
-    if (live) {
-#pragma unroll
-      for (int q = 0; q < M; ++q) base[(2 * q + half) * C::SY] = v[q];
-    }
-  }
-  __syncthreads();
-
-  // D: z c2r for crop (x, y) of my planes, row pairs (l, l + hl); bias + activation
-  const int L = nxl * a.vy;
-  const int hl = (L + 1) / 2;
-  const float bias = __ldg(a.bias + i);
-  for (int b0 = 0; b0 < hl; b0 += LINES) {
-    const int l1 = b0 + line;
-    const bool live = l1 < hl;
-    const int l2 = l1 + hl;
-    const bool has2 = live && l2 < L;
-    float2* s1 = sp + (xa - x0 + (live ? l1 / a.vy : 0)) * C::SX + (a.cy + (live ? l1 % a.vy : 0)) * C::SY;
-    float2* s2 = has2 ? sp + (xa - x0 + l2 / a.vy) * C::SX + (a.cy + l2 % a.vy) * C::SY : s1;
-    float2 zz[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-      const int k = half * M + q;
-      float2 A = make_float2(0.f, 0.f), B = make_float2(0.f, 0.f);
-      if (live) {
-        A = k < C::H ? s1[k] : s1[T - k];
-        if (has2) B = k < C::H ? s2[k] : s2[T - k];
-      }
-      zz[q] = k < C::H ? make_float2(A.x - B.y, A.y + B.x)     // A + iB
-                       : make_float2(A.x + B.y, -A.y + B.x);   // conj(A) + i conj(B)
-    }
-    fft_split2<T, true>(zz, half);
-    __syncwarp();  // the lane pair has read its rows before writing them
-    if (live) {
-      float* r1 = spf + 2 * (s1 - sp);
-      float* r2 = spf + 2 * (s2 - sp);
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        const int z = 2 * q + half;
-        if (z >= a.cz && z < a.cz + a.vz) {
-          const float v1 = zz[q].x + bias;
-          r1[z] = a.relu ? (v1 > 0.f ? v1 : 0.f) : v1;  // activate (layers.hpp:105-108)
-          if (has2) {
-            const float v2 = zz[q].y + bias;
-            r2[z] = a.relu ? (v2 > 0.f ? v2 : 0.f) : v2;
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  // E: store my crop planes, clipped to the output image (vz > 32: two lane passes)
-  for (int zb = 0; zb < T; zb += 32) {
-    const int lane = (tid & 31) + zb, warp = tid >> 5;
-    const int gy0 = ty * a.vy, gz = tz * a.vz + lane;
-    const bool zin = lane < a.vz && gz < a.onz;
-    const int ylim = min(a.vy, a.ony - gy0);
-    for (int xx = warp; xx < nxl; xx += NWARPS) {
-      const int gx = tx * a.vx + (xa - a.cx) + xx;
-      if (!zin || gx >= a.onx) continue;
-      float* o = a.dst + (s * a.fo + i) * a.oel + (int64_t(gx) * a.ony + gy0) * a.opz + gz;
-      const float* rr = spf + 2 * ((xa - x0 + xx) * C::SX + a.cy * C::SY) + a.cz + lane;
-#pragma unroll 4
-      for (int y = 0; y < ylim; ++y) {
-        *o = *rr;
-        o += a.opz;
-        rr += 2 * C::SY;
-      }
-    }
-  }
-}
-
 // T whose whole spectrum fits one CTA's shared memory (else: CTA pairs only)
 template <int T>
 constexpr bool single_fits() {
@@ -1171,17 +1018,7 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if ((T == 24 || T == 32) && a.lw == 16 && pair2_enabled()) {
-      static PerDeviceOnce p2conf;
-      if (p2conf.first()) {
-        VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_inv_pair2_kernel<T>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM_INV));
-      }
-      cfg.blockDim = dim3(Pair2Cfg<T>::THREADS);
-      VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair2_kernel<T>, a));
-    } else {
-      VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair_kernel<T>, a, ymap));
-    }
+    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_inv_pair_kernel<T>, a, ymap));
     c->counted();
     check_launch("tile_inv_pair_kernel");
     return;
