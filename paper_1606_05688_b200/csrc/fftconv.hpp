@@ -70,7 +70,6 @@ struct GemmArgs {
 extern const int kTileSizes[];
 // VXG_TILE_PAIR=0 disables the CTA-pair forward transform in planned layers
 bool tile_pair_enabled();
-bool pair2_enabled();  // VXG_PAIR2=1: forward pair transform with two threads per line
 bool inv_pair_enabled();  // VXG_INV_PAIR=0 disables the CTA-pair inverse
 extern const int kNumTileSizes;
 // frequencies of a T^3 tile padded to a multiple of the chunk width lw

@@ -429,193 +429,6 @@ __global__ void __launch_bounds__(PairCfg<T>::THREADS) tile_fwd_pair_kernel(FwdT
   cluster_wait();  // the peer finished reading my planes
 }
 
-// ---- K1 on a CTA pair, two threads per line --------------------------------------
-// The same transform as tile_fwd_pair_kernel with every line split over a
-// lane pair: lane h holds elements [h T/2, (h+1) T/2) of its line, one radix-2
-// DIF step across the pair (shfl.xor 1) leaves lane h with the T/2-point
-// problem whose outputs are the line's elements 2k + h.  Half the registers
-// per thread for twice the threads: more warps per SM to hide the passes'
-// shared-memory and DSMEM latencies.
-template <int T, bool INV>
-__device__ __forceinline__ void fft_split2(float2 (&v)[T / 2], int half) {
-  constexpr int M = T / 2;
-#pragma unroll
-  for (int j = 0; j < M; ++j) {
-    float2 p;
-    p.x = __shfl_xor_sync(0xffffffffu, v[j].x, 1);
-    p.y = __shfl_xor_sync(0xffffffffu, v[j].y, 1);
-    // half 0: a_j = x_j + x_{j+M}; half 1: b_j = (x_j - x_{j+M}) W_T^j
-    v[j] = half == 0 ? cadd(v[j], p) : twmul<T, INV>(csub(p, v[j]), j);
-  }
-  fft<M, INV>(v);
-}
-
-template <int T>
-struct Pair2Cfg {
-  using C = TileCfg<T>;
-  static constexpr int HP = T / 2;
-  static constexpr int WORK = HP * C::H > HP * HP ? HP * C::H : HP * HP;
-  static constexpr int THREADS = ((2 * WORK + 31) / 32) * 32;
-};
-
-template <int T>
-__global__ void __launch_bounds__(Pair2Cfg<T>::THREADS) tile_fwd_pair2_kernel(FwdTileArgs a) {
-  using C = TileCfg<T>;
-  using P = PairCfg<T>;
-  constexpr int HP = P::HP;
-  constexpr int M = T / 2;
-  constexpr int THREADS = Pair2Cfg<T>::THREADS;
-  constexpr int NWARPS = THREADS / 32;
-  extern __shared__ float2 sp[];
-  float* spf = reinterpret_cast<float*>(sp);
-  const unsigned r = cluster_rank();
-  const int64_t blk = blockIdx.x >> 1;
-  const int64_t j = blk % a.f;
-  const int64_t ml = blk / a.f;
-  const int64_t m = a.m0 + ml;
-  const int64_t s = m / a.tiles_per_img;
-  const int64_t t = m % a.tiles_per_img;
-  const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
-  const int ox = tx * a.vx + int(r) * HP, oy = ty * a.vy, oz = tz * a.vz;
-  const float* img = a.src + (s * a.f + j) * a.img_stride;
-  const int tid = threadIdx.x;
-  const int half = tid & 1, line = tid >> 1;
-
-  // A0: this CTA's planes (raw) -> slots, as tile_fwd_pair_kernel
-  for (int zb = 0; zb < T; zb += 32) {
-    const int lane = (tid & 31) + zb, warp = tid >> 5;
-    const int gz = oz + lane;
-    if (ox + HP <= a.nx && oy + T <= a.ny && oz + T <= a.nz) {
-      if (lane < T) {
-        for (int x = warp; x < HP; x += NWARPS) {
-          const float* g = img + (int64_t(ox + x) * a.ny + oy) * a.pz + gz;
-          float* d = spf + 2 * (x * C::SX) + lane;
-#pragma unroll 8
-          for (int y = 0; y < T; ++y) {
-            cp_async4(d + 2 * C::SY * y, g, true);
-            g += a.pz;
-          }
-        }
-      }
-    } else {
-      const bool zin = lane < T && gz < a.nz;
-      for (int x = warp; x < HP; x += NWARPS) {
-        const int gx = ox + x;
-        const bool xin = zin && gx < a.nx;
-        const float* g = img + (int64_t(gx) * a.ny + oy) * a.pz + gz;
-        float* d = spf + 2 * (x * C::SX) + lane;
-#pragma unroll 4
-        for (int y = 0; y < T; ++y) {
-          const bool in = xin && oy + y < a.ny;
-          if (lane < T) cp_async4(d, in ? g : img, in);
-          g += a.pz;
-          d += 2 * C::SY;
-        }
-      }
-    }
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-
-  // A1: z r2c, rows (x, y) and (x, y + T/2) share one complex transform; lane
-  // h holds z in [h M, (h+1) M) and ends with the outputs 2k + h -- a
-  // Hermitian pair (k, T - k) has one parity, so each lane unpacks its own
-  {
-    const bool live = line < HP * HP;
-    const int x = live ? line / HP : 0, y = live ? line % HP : 0;
-    float2* s1 = sp + x * C::SX + y * C::SY;
-    float2* s2 = s1 + HP * C::SY;
-    float2 zz[M];
-#pragma unroll
-    for (int q = 0; q < M / 2; ++q) {
-      const float2 r1 = live ? s1[half * (M / 2) + q] : make_float2(0.f, 0.f);
-      const float2 r2 = live ? s2[half * (M / 2) + q] : make_float2(0.f, 0.f);
-      zz[2 * q] = make_float2(r1.x, r2.x);
-      zz[2 * q + 1] = make_float2(r1.y, r2.y);
-    }
-    fft_split2<T, false>(zz, half);
-    __syncthreads();  // every lane has read its rows before the slots are overwritten
-    if (live) {
-#pragma unroll
-      for (int kk = 0; kk < (C::H + 1) / 2; ++kk) {
-        const int k = 2 * kk + half;
-        if (k < C::H) {
-          const float2 zk = zz[kk];
-          const float2 zn = cconj(half ? zz[M - kk - 1] : zz[(M - kk) % M]);
-          const float2 d = csub(zk, zn);
-          s1[k] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y + zn.y));
-          s2[k] = make_float2(0.5f * d.y, -0.5f * d.x);
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  // B: y lines (x, kz) of this CTA's planes
-  {
-    const bool live = line < HP * C::H;
-    const int kz = live ? line % C::H : 0, x = live ? line / C::H : 0;
-    float2* base = sp + x * C::SX + kz;
-    float2 v[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) v[q] = live ? base[(half * M + q) * C::SY] : make_float2(0.f, 0.f);
-    fft_split2<T, false>(v, half);
-    __syncthreads();  // all lines read before any is written back
-    if (live) {
-#pragma unroll
-      for (int q = 0; q < M; ++q) base[(2 * q + half) * C::SY] = v[q];
-    }
-  }
-  cluster_arrive();
-  cluster_wait();
-
-  // C: x lines (ky, kz) for ky in this CTA's half: lane h reads planes
-  // [h M, (h+1) M), its own CTA's when h == r, the peer's otherwise
-  const int lw = a.lw, lshift = __ffs(lw) - 1;
-  float2* dst = a.out + (ml * a.f + j) * lw;
-  const int64_t wb_stride = a.mstride * a.f * lw;
-  const bool live = line < HP * C::H;
-  float2 v[M];
-  {
-    const int ky = int(r) * HP + (live ? line / C::H : 0), kz = live ? line % C::H : 0;
-    const float2* base = sp + ky * C::SY + kz;
-    if (half == int(r)) {
-#pragma unroll
-      for (int q = 0; q < M; ++q) v[q] = live ? base[q * C::SX] : make_float2(0.f, 0.f);
-    } else {
-      const uint32_t pbase = peer_addr(base, r ^ 1u);
-#pragma unroll
-      for (int q = 0; q < M; ++q) v[q] = live ? ld_peer(pbase + uint32_t(q * C::SX * 8)) : make_float2(0.f, 0.f);
-    }
-  }
-  cluster_arrive();  // my reads of the peer are issued; it may exit after its own wait
-  fft_split2<T, false>(v, half);
-  if (live) {
-    const int t0 = int(r) * HP * C::H + line;  // w = kx*T*H + t0, kx = 2q + half
-    if ((T * C::H) % 16 == 0 && lw == 16) {
-      float2* o = dst + int64_t(t0 >> 4) * wb_stride + (t0 & 15);
-      const int64_t step = int64_t((T * C::H) / 16) * wb_stride;
-#pragma unroll
-      for (int q = 0; q < M; ++q) o[(2 * q + half) * step] = make_float2(v[q].x * a.scale, v[q].y * a.scale);
-    } else {
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        const int w = (2 * q + half) * T * C::H + t0;
-        dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = make_float2(v[q].x * a.scale, v[q].y * a.scale);
-      }
-    }
-  }
-  if (r == 0) {
-    const int nwp = ((C::NW + lw - 1) / lw) * lw;
-    if (tid < nwp - C::NW) {
-      const int w = C::NW + tid;
-      dst[int64_t(w >> lshift) * wb_stride + (w & (lw - 1))] = make_float2(0.f, 0.f);
-    }
-  }
-  cluster_wait();  // the peer finished reading my planes
-}
-
 // ---- K4: inverse tile transform with crop + bias + ReLU ------------------------
 template <int T>
 __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
@@ -948,17 +761,14 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
   using C = TileCfg<T>;
   if ((a.pair && T >= 24) || !single_fits<T>()) {
     using P = PairCfg<T>;
-    const bool two = (T == 24 || T == 32) && pair2_enabled();
     static PerDeviceOnce pconf;
     if (pconf.first()) {
       VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_pair_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
-      VXG_CUDA_CHECK(cudaFuncSetAttribute(tile_fwd_pair2_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(2 * nblocks));
-    cfg.blockDim = dim3(two ? Pair2Cfg<T>::THREADS : P::THREADS);
+    cfg.blockDim = dim3(P::THREADS);
     cfg.dynamicSmemBytes = P::SMEM;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
@@ -968,10 +778,7 @@ void fwd_t(Ctx* c, const FwdTileArgs& a, int64_t nblocks) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (two)
-      VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_fwd_pair2_kernel<T>, a));
-    else
-      VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_fwd_pair_kernel<T>, a));
+    VXG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tile_fwd_pair_kernel<T>, a));
     c->counted();
     check_launch("tile_fwd_pair_kernel");
     return;
@@ -1036,12 +843,6 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
 }
 
 }  // namespace
-
-// VXG_PAIR2=1: the forward pair transform with two threads per line (experiment)
-bool pair2_enabled() {
-  const char* e = std::getenv("VXG_PAIR2");
-  return e && std::strcmp(e, "0") != 0;
-}
 
 bool tile_pair_enabled() {
   static const bool on = [] {
