@@ -272,22 +272,28 @@ class DevBuf {
   void alloc(Ctx* c, i64 bytes) {
     reset();
     if (bytes <= 0) return;
+    i64 arena_largest = -1;
     if (c->arena) {
       void* q = nullptr;
+      Arena* ar = nullptr;
       {
         std::lock_guard<std::mutex> lk(c->mu);
-        q = c->arena->alloc(bytes);
+        ar = c->arena;
+        if (ar) {
+          q = ar->alloc(bytes);
+          if (!q) arena_largest = ar->largest();
+        }
       }
       if (q) {
-        c_ = c; p_ = q; n_ = bytes; arena_ = c->arena;
+        c_ = c; p_ = q; n_ = bytes; arena_ = ar;
         return;
       }
     }
     c->charge(bytes);
     void* p = nullptr;
-    if (trace_on() && c->arena)
+    if (trace_on() && arena_largest >= 0)
       std::fprintf(stderr, "[vxg] arena miss: %lld bytes from the pool (arena largest free %lld)\n",
-                   (long long)bytes, (long long)c->arena->largest());
+                   (long long)bytes, (long long)arena_largest);
     cudaError_t e = cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), c->pool, c->stream);
     if (e == cudaErrorMemoryAllocation) {
       if (trace_on()) std::fprintf(stderr, "[vxg] pool trim + remap for %lld bytes\n", (long long)bytes);

@@ -552,6 +552,7 @@ void Model::forward(const ForwardPlan& p, const float* d_in, float* d_dense, boo
       try {
         c->charge(arena_bytes);
       } catch (...) {
+        std::lock_guard<std::mutex> lk(c->mu);
         c->held_busy = false;
         throw;
       }
