@@ -266,26 +266,10 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    // NaN scan of the staged box (mpf_pool rejects NaN, layers.hpp:429): each
-    // staged element once, instead of per use in the window loop
-    // 16-byte reads; only a box reaching past nz masks its tail (the row
-    // padding is never written and may hold anything)
-    {
-      const int zlim = g.nz - z0;  // valid z in the box: [0, zlim)
-      const float4* b4 = reinterpret_cast<const float4*>(box);
-      for (int u = threadIdx.x; u < M2_BX * M2_BY * (M2_BZ / 4); u += 256) {
-        const float4 v = b4[u];
-        const int zc = 4 * (u % (M2_BZ / 4));
-        bool n = false;
-        if (zc + 3 < zlim) {
-          n = (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
-        } else {
-          n = ((v.x != v.x) && zc < zlim) | ((v.y != v.y) && zc + 1 < zlim) | ((v.z != v.z) && zc + 2 < zlim) |
-              ((v.w != v.w) && zc + 3 < zlim);
-        }
-        saw_nan |= n;
-      }
-    }
+    // NaN (mpf_pool rejects NaN, layers.hpp:429): checked on the values the
+    // window maxima read -- with an odd extent (every admissible MPF input)
+    // each input element lies in some window, so the live threads' reads
+    // cover the whole image; zero-filled staging outside it holds no NaN
     if (!live) continue;
     const int64_t s = plane / g.f;
     const int fm = int(plane % g.f);
@@ -313,6 +297,8 @@ __global__ void __launch_bounds__(256) mpf222_kernel(const float* __restrict__ i
       m1 = a2 > m1 ? a2 : m1;
       m1 = b01.y > m1 ? b01.y : m1;
       m1 = b2 > m1 ? b2 : m1;
+      saw_nan |= (a01.x != a01.x) | (a01.y != a01.y) | (b01.x != b01.x) | (b01.y != b01.y) | (a2 != a2) |
+                 (b2 != b2);
     };
     float p0, p1;
     rowmax(0, p0, p1);

@@ -466,3 +466,24 @@ def test_conv_fft_single_input_map_fused_inverse(oracle, ctx, T):
     b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
     got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=False, cta_pair=True, ctx=ctx)
     assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
+
+
+@pytest.mark.parametrize("mem", ["host", "device"])
+def test_mpf_rejects_nan_anywhere(ctx, mem):
+    """mpf_pool rejects a NaN wherever it sits (layers.hpp:429): the 2x2x2 kernel
+    checks the values its windows read, so every position class -- corners,
+    faces, the last plane of each axis, tile seams of its 16 x 8 x 64 staging --
+    must still be caught."""
+    import paper_1606_05688_b200 as v
+    n = (35, 19, 131)
+    rng = np.random.default_rng(9)
+    base = rng.uniform(-1, 1, (2, 3) + n).astype(np.float32)
+    put = _cuda if mem == "device" else (lambda a: a)
+    assert v.mpf_pool(put(base), (2, 2, 2), ctx).output is not None
+    for pos in [(0, 0, 0, 0, 0), (1, 2, 34, 18, 130), (0, 1, 34, 0, 0), (0, 0, 0, 18, 0), (1, 0, 0, 0, 130),
+                (0, 2, 16, 8, 64), (1, 1, 15, 7, 63), (0, 0, 17, 9, 65), (1, 2, 33, 17, 129)]:
+        x = base.copy()
+        x[pos] = np.nan
+        with pytest.raises(ValueError, match="NaN"):
+            v.mpf_pool(put(x), (2, 2, 2), ctx)
+    v.mpf_pool(put(base), (2, 2, 2), ctx)  # the flag was cleared
