@@ -64,7 +64,6 @@ def main():
         del x
     if "last" in a.which:
         # the 80 -> 3, k = 5 last layer of n537 at its bench fragment size
-        import os
         n = a.n if a.n != 256 else 76
         S = a.S if a.S != 1 else 64
         x = torch.rand((S, 80, n, n, n), device="cuda", generator=g) * 2 - 1
@@ -72,15 +71,12 @@ def main():
         b = torch.rand((3,), device="cuda", generator=g) * 0.2 - 0.1
         p = v.ConvLayerParams(w, b, "relu")
         for T in (12, 16, 24):
-            for fused in (1, 0):
-                os.environ["VXG_NO_FUSED_MAC"] = "0" if fused else "1"
-                ctx.profile(True)
-                t = timed(ctx, lambda: v.conv_fft_tiled(x, p, T, tensor_cores=False, ctx=ctx))
-                ks = ctx.kernel_stats()
-                ctx.profile(False)
-                res["last_80x3_k5_S%d_n%d_T%d_%s" % (S, n, T, "fused" if fused else "plain")] = {
-                    "s": t, "kernels": {k: round(s["seconds"] / s["launches"] * 1e3, 3) for k, s in ks.items()}}
-        os.environ.pop("VXG_NO_FUSED_MAC")
+            ctx.profile(True)
+            t = timed(ctx, lambda: v.conv_fft_tiled(x, p, T, tensor_cores=False, ctx=ctx))
+            ks = ctx.kernel_stats()
+            ctx.profile(False)
+            res["last_80x3_k5_S%d_n%d_T%d" % (S, n, T)] = {
+                "s": t, "kernels": {k: round(s["seconds"] / s["launches"] * 1e3, 3) for k, s in ks.items()}}
         del x
     if "direct" in a.which:
         n = 330
