@@ -57,7 +57,15 @@
 namespace vxg {
 
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                           const uint64_t* strides, const uint32_t* box);
+                           const uint64_t* strides, const uint32_t* box, bool swizzle128);
+
+// VXG_Q_SWZ=1: X boxes of 8 channel lines with the 128-byte swizzle instead of
+// 9 lines (144-byte staged rows); both are conflict-free for the converters,
+// the swizzled box reads 1/9 fewer bytes through L2
+bool q_x_swizzle() {
+  const char* e = std::getenv("VXG_Q_SWZ");
+  return e && std::strcmp(e, "1") == 0;
+}
 
 // VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
 // tf32 + bf16-correction pair (the W layout follows the same switch)
@@ -70,7 +78,7 @@ namespace {
 
 using namespace tc;
 constexpr int Q_THREADS = 512;  // 16 warps
-constexpr int Q_RAW_ROW = 144;  // 9 channel pieces of 16 B per staged row
+constexpr int Q_RAW_ROW = 144;  // staged row: 9 channel pieces of 16 B, or 8 swizzled (128 B)
 constexpr int Q_RAW = TC_M * Q_RAW_ROW;
 
 template <int FO>
@@ -295,6 +303,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       long long t1 = a.prof ? clock64() : 0;
       cw += t1 - t0;
       const uint8_t* raw = smem + s * Q_RAW + c * a.raw_row;
+      // swizzled box (raw_row = 128): piece ch of row c sits at 16 * (ch ^ (c & 7))
+      const int sw = a.raw_row == 128 ? (c & 7) : 0;
       // split X row c into tf32 hi/lo: A slot columns ((w*2 + comp)*2 + hi/lo)*8 + channel
       // (BFC: the lo part's 8 columns hold the packed bf16 correction operand:
       // columns 0-3 bf16(hi) of channels (0,1)..(6,7), columns 4-7 bf16(lo))
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       (void)hl;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        const float4 v = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
+        const float4 v = *reinterpret_cast<const float4*>(raw + (ch ^ sw) * 16);  // (re0, im0, re1, im1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float x = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -542,13 +552,16 @@ void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
   // 9 channel lines per box (the 9th pads a staged row to 144 B: conflict-free
   // converter reads; zero-filled past the last channel); a box may not exceed
   // the tensor, so fewer channels / rows when the layer is that small
-  const uint32_t bch = uint32_t(std::min(9, g.f)), brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
+  // swizzled: 8 lines, piece ch of row r at 16 * (ch ^ (r & 7)) in a 128-byte
+  // staged row (ring slots are 1024-byte aligned, as the swizzle requires)
+  const bool swz = q_x_swizzle();
+  const uint32_t bch = swz ? 8u : uint32_t(std::min(9, g.f)), brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
   const uint32_t box[4] = {4, bch, brows, 1};
-  a.raw_row = int(16 * bch);
+  a.raw_row = swz ? 128 : int(16 * bch);
   a.raw_bytes = int(16 * bch * brows);
   static const int dbg = std::getenv("VXG_TC_DBG") ? std::atoi(std::getenv("VXG_TC_DBG")) : 0;
   a.dbg = dbg;
-  encode_tensor_map_f32(&xmap, g.X, 4, dims, strides, box);
+  encode_tensor_map_f32(&xmap, g.X, 4, dims, strides, box, swz);
   const int64_t ntiles = a.nwb * a.mblocks * 8;
   const unsigned grid = unsigned(std::min<int64_t>(ntiles, c->num_sms));
   static const bool prof = std::getenv("VXG_TC_PROF") != nullptr;
@@ -605,6 +618,7 @@ bool tc_quad_enabled() {
 }
 
 int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
+  if (q2_enabled()) return q2_wsplit_bytes(npairs, f, fo);
   // per (pair, half, chunk): 2 frequencies x hi/lo x 3 blocks x (fo/2) x 8 tf32
   return npairs * 2 * (f / TC_KC) * 4 * 3 * (fo / 2) * TC_KC * 4;
 }
@@ -620,6 +634,7 @@ int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
   }
 
 void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo) {
+  if (q2_enabled()) return q2_wsplit(c, raw, out, npairs, f, fo);
   KScope ks(c, VXG_K_KSPEC, 0.0, double(npairs) * 2 * f * fo * (16.0 + 24.0));
 #define VXG_QW(F) q_wsplit_t<F>(c, raw, out, npairs, int(f))
   VXG_Q_SWITCH(VXG_QW)
@@ -627,6 +642,7 @@ void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, i
 }
 
 void launch_cgemm_q(Ctx* c, const GemmArgs& a, int64_t npairs) {
+  if (q2_enabled()) return launch_cgemm_q2(c, a, npairs);
   const double nw = double(a.T) * a.T * (a.T / 2 + 1);
   KScope ks(c, VXG_K_CGEMM, 8.0 * double(a.M) * a.f * a.fo * nw,
             8.0 * nw * (double(a.M) * a.f + double(a.M) * a.fo + double(a.f) * a.fo));
