@@ -93,12 +93,6 @@ bool q_bf16_correction();
 int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
 void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
 void launch_cgemm_q(Ctx* c, const GemmArgs& a, int64_t npairs);
-// the quad contraction on CTA pairs (k_cgemm_q2.cu, tcgen05 cta_group::2); its
-// own W layout, selected together with the kernel (VXG_Q2=0: single-CTA)
-bool q2_enabled();
-int64_t q2_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo);
-void q2_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo);
-void launch_cgemm_q2(Ctx* c, const GemmArgs& a, int64_t npairs);
 
 // Tile-size choice for a layer: minimises the modelled cost of transforms +
 // contraction over the supported sizes (or honours T_forced > 0).

@@ -438,8 +438,7 @@ struct Runner {
 const float2* Model::spectra_for(int ci, const FftPlan& plan, bool /*cache*/) {
   const int T = plan.T;
   auto key = std::make_pair(ci, (T << 8) | (plan.tc ? 1 : 0) | (plan.tc && plan.quad ? 2 : 0) |
-                                    (plan.tc && plan.quad && q_bf16_correction() ? 4 : 0) |
-                                    (plan.tc && plan.quad && q2_enabled() ? 8 : 0));
+                                    (plan.tc && plan.quad && q_bf16_correction() ? 4 : 0));
   auto it = spectra.find(key);
   if (it != spectra.end()) return it->second.as<float2>();
   int64_t f = net.fin;

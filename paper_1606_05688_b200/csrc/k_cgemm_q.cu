@@ -59,12 +59,14 @@ namespace vxg {
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                            const uint64_t* strides, const uint32_t* box, bool swizzle128);
 
-// VXG_Q_SWZ=1: X boxes of 8 channel lines with the 128-byte swizzle instead of
-// 9 lines (144-byte staged rows); both are conflict-free for the converters,
-// the swizzled box reads 1/9 fewer bytes through L2
+// X boxes of 8 channel lines landed with the TMA 128-byte swizzle (piece ch of
+// staged row r at 16 * (ch ^ (r & 7))); VXG_Q_SWZ=0 restores 9-line boxes
+// (144-byte rows).  Both are conflict-free for the converters; the swizzled box
+// reads 1/9 fewer bytes through L2, the kernel's binding resource (kbench 80 ->
+// 80 k5, S = 64, n = 85, T = 32: 13.9 -> 12.8 ms)
 bool q_x_swizzle() {
   const char* e = std::getenv("VXG_Q_SWZ");
-  return e && std::strcmp(e, "1") == 0;
+  return !(e && std::strcmp(e, "0") == 0);
 }
 
 // VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
@@ -618,7 +620,6 @@ bool tc_quad_enabled() {
 }
 
 int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
-  if (q2_enabled()) return q2_wsplit_bytes(npairs, f, fo);
   // per (pair, half, chunk): 2 frequencies x hi/lo x 3 blocks x (fo/2) x 8 tf32
   return npairs * 2 * (f / TC_KC) * 4 * 3 * (fo / 2) * TC_KC * 4;
 }
@@ -634,7 +635,6 @@ int64_t q_wsplit_bytes(int64_t npairs, int64_t f, int64_t fo) {
   }
 
 void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, int64_t fo) {
-  if (q2_enabled()) return q2_wsplit(c, raw, out, npairs, f, fo);
   KScope ks(c, VXG_K_KSPEC, 0.0, double(npairs) * 2 * f * fo * (16.0 + 24.0));
 #define VXG_QW(F) q_wsplit_t<F>(c, raw, out, npairs, int(f))
   VXG_Q_SWITCH(VXG_QW)
@@ -642,7 +642,6 @@ void q_wsplit(Ctx* c, const float2* raw, void* out, int64_t npairs, int64_t f, i
 }
 
 void launch_cgemm_q(Ctx* c, const GemmArgs& a, int64_t npairs) {
-  if (q2_enabled()) return launch_cgemm_q2(c, a, npairs);
   const double nw = double(a.T) * a.T * (a.T / 2 + 1);
   KScope ks(c, VXG_K_CGEMM, 8.0 * double(a.M) * a.f * a.fo * nw,
             8.0 * nw * (double(a.M) * a.f + double(a.M) * a.fo + double(a.f) * a.fo));

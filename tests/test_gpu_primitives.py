@@ -489,35 +489,12 @@ def test_mpf_rejects_nan_anywhere(ctx, mem):
     v.mpf_pool(put(base), (2, 2, 2), ctx)  # the flag was cleared
 
 
-@pytest.mark.parametrize("S,f,fo,n,T", [(2, 80, 80, 70, 32), (1, 16, 32, 40, 16), (3, 24, 48, 30, 24),
-                                        (1, 8, 16, 20, 8)])
-def test_conv_fft_cta_pair_contraction_matches_single_cta(ctx, monkeypatch, S, f, fo, n, T):
-    """The quad contraction on CTA pairs (k_cgemm_q2.cu: cta_group::2, M = 256
-    rows per MMA, the kernel-spectrum operand split by columns across the two
-    SMs) against the single-CTA quad kernel (VXG_Q2=0) on the same inputs,
-    incl. layers with fewer than 256 (and 128) spectrum rows."""
-    import torch
-    import paper_1606_05688_b200 as v
-    g = torch.Generator(device="cuda").manual_seed(S * 7 + f + fo + n + T)
-    x = torch.rand((S, f, n, n, n), device="cuda", generator=g) * 2 - 1
-    w = (torch.rand((fo, f, 5, 5, 5), device="cuda", generator=g) * 2 - 1) * (3.0 / (f * 125)) ** 0.5
-    b = (torch.rand((fo,), device="cuda", generator=g) * 2 - 1) * 0.1
-    p = v.ConvLayerParams(w.contiguous(), b.contiguous(), "identity")
-    monkeypatch.setenv("VXG_Q2", "1")
-    pair = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
-    monkeypatch.setenv("VXG_Q2", "0")
-    single = v.conv_fft_tiled(x, p, T, tensor_cores=True, ctx=ctx)
-    err = ((pair - single).abs().max() / single.abs().max()).item()
-    assert err <= 1e-6, err
-
-
 @pytest.mark.parametrize("swz", ["0", "1"])
 def test_conv_fft_quad_tiles_x_box_layouts(oracle, ctx, monkeypatch, swz):
     """The single-CTA quad contraction with either staged X layout (9 channel
-    lines per row, or 8 lines with the TMA 128-byte swizzle, VXG_Q_SWZ=1)
+    lines per row (VXG_Q_SWZ=0), or 8 lines with the TMA 128-byte swizzle)
     against the C oracle."""
     import paper_1606_05688_b200 as v
-    monkeypatch.setenv("VXG_Q2", "0")
     monkeypatch.setenv("VXG_Q_SWZ", swz)
     S, f, fo, k, T = 2, 24, 32, (3, 3, 3), 16
     n = (T + 9, 2 * T - 1, T + 4)
