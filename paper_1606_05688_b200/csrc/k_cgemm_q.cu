@@ -57,17 +57,7 @@
 namespace vxg {
 
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                           const uint64_t* strides, const uint32_t* box, bool swizzle128);
-
-// X boxes of 8 channel lines landed with the TMA 128-byte swizzle (piece ch of
-// staged row r at 16 * (ch ^ (r & 7))); VXG_Q_SWZ=0 restores 9-line boxes
-// (144-byte rows).  Both are conflict-free for the converters; the swizzled box
-// reads 1/9 fewer bytes through L2, the kernel's binding resource (kbench 80 ->
-// 80 k5, S = 64, n = 85, T = 32: 13.9 -> 12.8 ms)
-bool q_x_swizzle() {
-  const char* e = std::getenv("VXG_Q_SWZ");
-  return !(e && std::strcmp(e, "0") == 0);
-}
+                           const uint64_t* strides, const uint32_t* box);
 
 // VXG_Q_3TF32=1: the full 3xTF32 split (3 MMAs per product) instead of the
 // tf32 + bf16-correction pair (the W layout follows the same switch)
@@ -80,7 +70,7 @@ namespace {
 
 using namespace tc;
 constexpr int Q_THREADS = 512;  // 16 warps
-constexpr int Q_RAW_ROW = 144;  // staged row: 9 channel pieces of 16 B, or 8 swizzled (128 B)
+constexpr int Q_RAW_ROW = 144;  // 9 channel pieces of 16 B per staged row
 constexpr int Q_RAW = TC_M * Q_RAW_ROW;
 
 template <int FO>
@@ -305,8 +295,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       long long t1 = a.prof ? clock64() : 0;
       cw += t1 - t0;
       const uint8_t* raw = smem + s * Q_RAW + c * a.raw_row;
-      // swizzled box (raw_row = 128): piece ch of row c sits at 16 * (ch ^ (c & 7))
-      const int sw = a.raw_row == 128 ? (c & 7) : 0;
       // split X row c into tf32 hi/lo: A slot columns ((w*2 + comp)*2 + hi/lo)*8 + channel
       // (BFC: the lo part's 8 columns hold the packed bf16 correction operand:
       // columns 0-3 bf16(hi) of channels (0,1)..(6,7), columns 4-7 bf16(lo))
@@ -315,7 +303,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       (void)hl;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        const float4 v = *reinterpret_cast<const float4*>(raw + (ch ^ sw) * 16);  // (re0, im0, re1, im1)
+        const float4 v = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float x = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -554,16 +542,13 @@ void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
   // 9 channel lines per box (the 9th pads a staged row to 144 B: conflict-free
   // converter reads; zero-filled past the last channel); a box may not exceed
   // the tensor, so fewer channels / rows when the layer is that small
-  // swizzled: 8 lines, piece ch of row r at 16 * (ch ^ (r & 7)) in a 128-byte
-  // staged row (ring slots are 1024-byte aligned, as the swizzle requires)
-  const bool swz = q_x_swizzle();
-  const uint32_t bch = swz ? 8u : uint32_t(std::min(9, g.f)), brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
+  const uint32_t bch = uint32_t(std::min(9, g.f)), brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
   const uint32_t box[4] = {4, bch, brows, 1};
-  a.raw_row = swz ? 128 : int(16 * bch);
+  a.raw_row = int(16 * bch);
   a.raw_bytes = int(16 * bch * brows);
   static const int dbg = std::getenv("VXG_TC_DBG") ? std::atoi(std::getenv("VXG_TC_DBG")) : 0;
   a.dbg = dbg;
-  encode_tensor_map_f32(&xmap, g.X, 4, dims, strides, box, swz);
+  encode_tensor_map_f32(&xmap, g.X, 4, dims, strides, box);
   const int64_t ntiles = a.nwb * a.mblocks * 8;
   const unsigned grid = unsigned(std::min<int64_t>(ntiles, c->num_sms));
   static const bool prof = std::getenv("VXG_TC_PROF") != nullptr;

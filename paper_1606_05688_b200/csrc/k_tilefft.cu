@@ -52,7 +52,7 @@ void init_twiddles() {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                           const uint64_t* strides, const uint32_t* box, bool swizzle128) {
+                           const uint64_t* strides, const uint32_t* box) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -69,8 +69,7 @@ void encode_tensor_map_f32(CUtensorMap* m, const void* base, int rank, const uin
     if (k < rank - 1) st[k] = strides[k];
   }
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<void*>(base), d, st,
-                         bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                         bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw cuda_failure("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
@@ -812,7 +811,7 @@ void inv_t(Ctx* c, const InvTileArgs& a, int64_t nblocks) {
       const uint64_t dims[4] = {4, uint64_t(a.fo), uint64_t(a.mstride), uint64_t(a.nwp) / 2};
       const uint64_t strides[3] = {16, uint64_t(a.fo) * 16, uint64_t(a.mstride) * a.fo * 16};
       const uint32_t box[4] = {4, 1, 1, uint32_t(P::HP * TileCfg<T>::H / 2)};
-      encode_tensor_map_f32(&ymap, a.spec, 4, dims, strides, box, false);
+      encode_tensor_map_f32(&ymap, a.spec, 4, dims, strides, box);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(2 * nblocks));

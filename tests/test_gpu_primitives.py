@@ -488,19 +488,3 @@ def test_mpf_rejects_nan_anywhere(ctx, mem):
             v.mpf_pool(put(x), (2, 2, 2), ctx)
     v.mpf_pool(put(base), (2, 2, 2), ctx)  # the flag was cleared
 
-
-@pytest.mark.parametrize("swz", ["0", "1"])
-def test_conv_fft_quad_tiles_x_box_layouts(oracle, ctx, monkeypatch, swz):
-    """The single-CTA quad contraction with either staged X layout (9 channel
-    lines per row (VXG_Q_SWZ=0), or 8 lines with the TMA 128-byte swizzle)
-    against the C oracle."""
-    import paper_1606_05688_b200 as v
-    monkeypatch.setenv("VXG_Q_SWZ", swz)
-    S, f, fo, k, T = 2, 24, 32, (3, 3, 3), 16
-    n = (T + 9, 2 * T - 1, T + 4)
-    rng = np.random.default_rng(41)
-    x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
-    w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 27))).astype(np.float32)
-    b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
-    got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=True, ctx=ctx)
-    assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
