@@ -27,11 +27,11 @@
 //
 // Persistent, warp-specialised pipeline over items (tile, pass, K chunk of 8
 // input maps), handshakes on mbarriers:
-//   warp 0 lane 0  X producer: one TMA box per item (the pass's 16-byte piece
-//                  of 128 rows x 9 channel lines; the 9th pads a staged row to
-//                  144 B so the converters' reads are conflict-free) into a
-//                  ring of 5 boxes (fo = 80), freed by the converters as soon
-//                  as they hold the box in registers;
+//   warp 0 lane 0  X producer: per item one TMA box per channel line (the
+//                  pass's 16-byte piece of 128 rows), staged [channel][row]
+//                  so a converter thread per row reads conflict-free, into a
+//                  ring of 6 items (fo = 80), freed by the converters as soon
+//                  as they hold the item in registers;
 //   warp 2 lane 0  W producer: one bulk copy of the item's pre-split W
 //                  (written once per layer by q_wsplit_kernel) into a 3-deep
 //                  ring shared with the TMEM A slots;
@@ -70,8 +70,10 @@ namespace {
 
 using namespace tc;
 constexpr int Q_THREADS = 512;  // 16 warps
-constexpr int Q_RAW_ROW = 144;  // 9 channel pieces of 16 B per staged row
-constexpr int Q_RAW = TC_M * Q_RAW_ROW;
+// staged X box: [channel][row][16 B] (one TMA box per channel line), so a
+// converter thread per row reads conflict-free; row-major staging needed a 9th
+// padding line per row (1/9 more L2 reads, 7-9 % slower, profiles/r2_experiments.md §14)
+constexpr int Q_RAW = TC_KC * TC_M * 16;
 
 template <int FO>
 struct QCfg {
@@ -166,7 +168,6 @@ struct QArgs {
   int64_t M, mstride;
   int f, fo, mblocks;
   int64_t nwb;
-  int raw_row;      // staged row stride (16 B x box channels)
   int raw_bytes;    // bytes one X box lands in shared memory
   int dbg;          // VXG_TC_DBG experiment switches, results invalid when set:
                     // 2 skip the Y stores, 4 skip the epilogue's TMEM loads, 8 skip the A stores
@@ -257,14 +258,15 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
             if (wrapped) mbar_wait(xp ? &rfree[s] : &aempty[s], ph ^ 1u);
             if (a.prof) pw += clock64() - t0;
             if (xp) {
-              // X: floats [q*8 + pass*4, +4) of 9 channel lines from kc*8, 128 rows
+              // X: floats [q*8 + pass*4, +4) of the 8 channel lines from kc*8, 128 rows
               mbar_arrive_expect_tx(&rfull[s], a.raw_bytes);
-              asm volatile(
-                  "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-                  "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(smem + s * Q_RAW)),
-                  "l"(&xmap), "r"(q * 8 + pass * 4), "r"(kc * TC_KC), "r"(int(m0)), "r"(int(wb)),
-                  "r"(smem_u32(&rfull[s]))
-                  : "memory");
+              for (int ch = 0; ch < TC_KC; ++ch)
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                    "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(smem + s * Q_RAW + ch * TC_M * 16)),
+                    "l"(&xmap), "r"(q * 8 + pass * 4), "r"(kc * TC_KC + ch), "r"(int(m0)), "r"(int(wb)),
+                    "r"(smem_u32(&rfull[s]))
+                    : "memory");
             } else {
               const int64_t pair = wb * 8 + q * 2 + pass;
               mbar_arrive_expect_tx(&wfull[s], C::WITEM);
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       mbar_wait(&rfull[s], ph);
       long long t1 = a.prof ? clock64() : 0;
       cw += t1 - t0;
-      const uint8_t* raw = smem + s * Q_RAW + c * a.raw_row;
+      const uint8_t* raw = smem + s * Q_RAW + c * 16;
       // split X row c into tf32 hi/lo: A slot columns ((w*2 + comp)*2 + hi/lo)*8 + channel
       // (BFC: the lo part's 8 columns hold the packed bf16 correction operand:
       // columns 0-3 bf16(hi) of channels (0,1)..(6,7), columns 4-7 bf16(lo))
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       (void)hl;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        const float4 v = *reinterpret_cast<const float4*>(raw + ch * 16);  // (re0, im0, re1, im1)
+        const float4 v = *reinterpret_cast<const float4*>(raw + ch * (TC_M * 16));  // (re0, im0, re1, im1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float x = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -539,13 +541,11 @@ void q_t(Ctx* c, const GemmArgs& g, int64_t npairs) {
   CUtensorMap xmap;
   const uint64_t dims[4] = {32, uint64_t(g.f), uint64_t(g.mstride), uint64_t(a.nwb)};
   const uint64_t strides[3] = {128, uint64_t(g.f) * 128, uint64_t(g.mstride) * g.f * 128};
-  // 9 channel lines per box (the 9th pads a staged row to 144 B: conflict-free
-  // converter reads; zero-filled past the last channel); a box may not exceed
-  // the tensor, so fewer channels / rows when the layer is that small
-  const uint32_t bch = uint32_t(std::min(9, g.f)), brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
-  const uint32_t box[4] = {4, bch, brows, 1};
-  a.raw_row = int(16 * bch);
-  a.raw_bytes = int(16 * bch * brows);
+  // one box per channel line: 4 floats x 128 rows (fewer rows when the layer
+  // is that small: a box may not exceed the tensor)
+  const uint32_t brows = uint32_t(std::min<int64_t>(TC_M, g.mstride));
+  const uint32_t box[4] = {4, 1, brows, 1};
+  a.raw_bytes = int(16 * TC_KC * brows);
   static const int dbg = std::getenv("VXG_TC_DBG") ? std::atoi(std::getenv("VXG_TC_DBG")) : 0;
   a.dbg = dbg;
   encode_tensor_map_f32(&xmap, g.X, 4, dims, strides, box);

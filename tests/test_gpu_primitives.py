@@ -488,3 +488,20 @@ def test_mpf_rejects_nan_anywhere(ctx, mem):
             v.mpf_pool(put(x), (2, 2, 2), ctx)
     v.mpf_pool(put(base), (2, 2, 2), ctx)  # the flag was cleared
 
+
+
+
+def test_conv_fft_quad_tiles_short_layers(oracle, ctx):
+    """The quad contraction on layers with fewer than 128 spectrum rows (its X
+    boxes then cover only the rows the tensor has) and with the widest map
+    count, against the C oracle."""
+    import paper_1606_05688_b200 as v
+    rng = np.random.default_rng(41)
+    for S, f, fo, T in ((2, 24, 32, 16), (1, 16, 80, 24)):
+        k = (3, 3, 3)
+        n = (T + 9, 2 * T - 1, T + 4) if S > 1 else (T + 2,) * 3
+        x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
+        w = (rng.uniform(-1, 1, (fo, f) + k) * np.sqrt(3.0 / (f * 27))).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
+        got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=True, ctx=ctx)
+        assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4, (S, f, fo, T)
