@@ -34,10 +34,10 @@ NET = "n537"
 SMALLEST = {"n337": 92, "n537": 170, "n726": 120, "n926": 158}
 # ncu dram__bytes_read.sum + dram__bytes_write.sum / algorithmic bytes of one
 # cgemm_q_kernel<80, 1> launch (kbench 80 -> 80 k5, S = 64, n = 85, T = 32, 1728
-# rows: 23.44 + 19.21 GB against 8 * 17408 * (2 * 1728 * 80 + 80 * 80) B = 39.39 GB),
-# profiles/r2/r2z_layer_full.txt
-TRAFFIC_RATIO = {"cgemm": round((23.444 + 19.212) / 39.394, 3)}
-TRAFFIC_SOURCE = "profiles/r2/r2z_layer_full.txt"
+# rows: 24.14 + 19.22 GB against 8 * 17408 * (2 * 1728 * 80 + 80 * 80) B = 39.39 GB),
+# profiles/r2/h3_layer_full.txt
+TRAFFIC_RATIO = {"cgemm": round((24.143 + 19.217) / 39.394, 3)}
+TRAFFIC_SOURCE = "profiles/r2/h3_layer_full.txt"
 FFMA_FALLBACK_TFLOPS = 74.4  # 148 SM x 128 x 2 x 1.965 GHz (nominal), used only if measurement fails
 
 
