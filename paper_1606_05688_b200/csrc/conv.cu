@@ -83,9 +83,12 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.lw = 16;
     p.tc = tc;
     p.quad = tc_quad_enabled();
-    // measured wins (other T <= 32: one CTA is as fast); T >= 36 runs on pairs only
-    p.pair = ((T == 32 || T == 24) && tile_pair_enabled()) || T >= 36;
-    p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 36;
+    // measured wins: pairs at T = 24 / 32; one CTA at the other sizes it fits,
+    // T = 36 included (199 KB of shared memory, one CTA per SM: 1.31 vs 1.44 ns
+    // per output voxel on the CTA pair for 80 -> 80 k7, profiles/r2_experiments.md
+    // §15); T = 40 exceeds one CTA's shared memory and runs on pairs only
+    p.pair = ((T == 32 || T == 24) && tile_pair_enabled()) || T >= 40;
+    p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 40;
     p.ylw = (tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
     p.nwp = tile_nwp(T, p.lw);
     p.fused_f1 = f == 1 && p.inv_pair && !p.tc && fused_f1_enabled();
@@ -98,7 +101,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     const double flops = 8.0 * M * double(f) * double(fo) * nw;
     const double cta = 140e-9 * std::pow(double(T) / 32.0, 3.0) * std::log2(double(T)) / 5.0;
     const double bytes = 16.0 * M * double(f + fo) * nw;
-    // T = 36 / 40 run on CTA pairs at one pair per SM: measured ~1.5x the
+    // T = 36 (one CTA) / 40 (CTA pairs) run one CTA per SM: measured ~1.5x the
     // per-(tile, channel) time the T^3 log T scaling predicts
     const double big = T >= 36 ? 1.5 : 1.0;
     p.cost = flops / (tc ? 150e12 : 40e12) + M * double(f + fo) * cta * big + bytes / 5e12;

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--net", default="n537")
     ap.add_argument("--extent", type=int, default=722)
     ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--k", type=int, default=7)
     a = ap.parse_args()
     ctx = v.Context(0)
     res = {}
@@ -77,6 +78,23 @@ def main():
             ctx.profile(False)
             res["last_80x3_k5_S%d_n%d_T%d" % (S, n, T)] = {
                 "s": t, "kernels": {k: round(s["seconds"] / s["launches"] * 1e3, 3) for k, s in ks.items()}}
+        del x
+    if "tiles" in a.which:
+        # one 80 -> 80 layer (kernel a.k) at tile size a.T: one CTA vs CTA-pair transforms
+        n, kk = a.n, a.k
+        x = torch.rand((a.S, 80, n, n, n), device="cuda", generator=g) * 2 - 1
+        w = (torch.rand((80, 80, kk, kk, kk), device="cuda", generator=g) * 2 - 1) * 0.02
+        b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
+        p = v.ConvLayerParams(w, b, "relu")
+        for pair in (False, True):
+            ctx.profile(True)
+            t = timed(ctx, lambda: v.conv_fft_tiled(x, p, a.T, tensor_cores=True, cta_pair=pair, ctx=ctx))
+            ks = ctx.kernel_stats()
+            ctx.profile(False)
+            no = n - kk + 1
+            res["tiles_80x80_k%d_S%d_n%d_T%d_%s" % (kk, a.S, n, a.T, "pair" if pair else "single")] = {
+                "s": t, "ns_per_vox": t / (a.S * no ** 3) * 1e9,
+                "kernels": {k2: round(s2["seconds"] * 1e3, 2) for k2, s2 in ks.items()}}
         del x
     if "direct" in a.which:
         n = 330
