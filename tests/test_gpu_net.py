@@ -196,7 +196,16 @@ def _bench_plan(name, ctx):
     net = v.parse_network_spec(NETS[name])
     fov = FOV[name]
     model = v.Model(net, v.random_weights(net, 1), ctx)
-    budget = ctx.memory()["budget"] - ctx.memory()["current"]
+    # the context's budget was fixed when the session's context was made; tensors
+    # torch still caches from earlier tests are outside it, so also cap by what
+    # the device has free now (bench.py runs in a fresh process: budget only)
+    import gc
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+    ctx.trim()
+    budget = min(ctx.memory()["budget"] - ctx.memory()["current"],
+                 torch.cuda.mem_get_info()[0] - (3 << 30))
     e, _ = bench.choose_patch(model, net, fov, budget, False)
     model.tune(1, e)
     e, algos = bench.choose_patch(model, net, fov, budget, True)
@@ -317,7 +326,11 @@ def test_run_bench_csv_matches_the_reference_columns(tmp_path):
     spec = importlib.util.spec_from_file_location("run_bench", root / "tools" / "run_bench.py")
     rb = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(rb)
+    import gc
+    import torch
     import paper_1606_05688_b200 as v
+    gc.collect()
+    torch.cuda.empty_cache()  # tensors earlier tests left in torch's cache
     budget = v.default_context().memory()["budget"]
     out = tmp_path / "bench.csv"
     assert rb.main(["--net", "n337", "--min-extent", "92", "--max-extent", "108", "--csv", str(out)]) == 0

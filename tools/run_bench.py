@@ -58,7 +58,11 @@ def main(argv=None) -> int:
     hi = a.max_extent or lo + 64
     ctx = v.Context(0)
     model = v.Model(net, v.random_weights(net, a.seed), ctx)
-    budget = ctx.memory()["budget"]
+    # the context budget, capped by what the device has free now (another
+    # context or torch's cache in the same process may hold memory outside it)
+    torch.cuda.empty_cache()
+    ctx.trim()
+    budget = min(ctx.memory()["budget"] - ctx.memory()["current"], torch.cuda.mem_get_info()[0] - (2 << 30))
     out = open(a.csv, "w") if a.csv else sys.stdout
     note = sys.stdout if a.csv else sys.stderr  # cli.cpp:235: notes beside the rows
     note.write(f"seed {a.seed}\n")
