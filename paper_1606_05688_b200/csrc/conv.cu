@@ -91,7 +91,7 @@ FftPlan plan_fft(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T_forced) {
     p.inv_pair = ((T == 32 || T == 24) && tile_pair_enabled() && inv_pair_enabled()) || T >= 40;
     p.ylw = (tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
     p.nwp = tile_nwp(T, p.lw);
-    p.fused_f1 = f == 1 && p.inv_pair && !p.tc && fused_f1_enabled();
+    p.fused_f1 = f == 1 && !p.tc && fused_f1_enabled();
     const double M = double(S) * double(p.tiles);
     const double nw = double(T) * T * (T / 2 + 1);
     // Modelled seconds (calibrated on B200 with tools/kbench.py): the
@@ -121,7 +121,7 @@ FftPlan plan_fft_forced(V3 n, V3 k, int64_t f, int64_t fo, int64_t S, int T, boo
   p.lw = 16;
   p.ylw = (p.tc && p.inv_pair && ypair_enabled()) ? 2 : 16;
   p.nwp = tile_nwp(T, p.lw);
-  p.fused_f1 = f == 1 && p.inv_pair && !p.tc && fused_f1_enabled();
+  p.fused_f1 = f == 1 && !p.tc && fused_f1_enabled();
   return p;
 }
 

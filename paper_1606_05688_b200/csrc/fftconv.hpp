@@ -109,7 +109,7 @@ struct FftPlan {
                      // 2 frequencies x all maps (k_cgemm_tc.cu); the measured planner picks
   bool pair = false;     // forward tile transform on a CTA pair (T >= 24)
   bool inv_pair = false; // inverse tile transform on a CTA pair (T >= 24)
-  bool fused_f1 = false; // f = 1, FFMA: the elementwise contraction happens in the inverse's loads (no Y)
+  bool fused_f1 = false; // f = 1, FFMA: the elementwise contraction happens in the inverse's loads (no Y; one CTA or pair)
   int64_t nwp = 0;   // padded frequencies per (row, channel)
   double cost = 0;
 };

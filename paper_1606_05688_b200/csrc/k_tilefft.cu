@@ -445,11 +445,12 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const int tz = int(t % a.ntz), ty = int((t / a.ntz) % a.nty), tx = int(t / (int64_t(a.ntz) * a.nty));
   const int tid = threadIdx.x;
 
-  // A: spectrum lines -> smem (asynchronous 8-byte copies)
+  // A: spectrum lines -> smem (asynchronous 8-byte copies); with a single
+  // input map (a.wsp) the x pass forms Y = X W from HBM itself instead
   const int lw = a.lw, lshift = __ffs(lw) - 1;
   const float2* src = a.spec + (ml * a.fo + i) * lw;
   const int64_t wb_stride = a.mstride * a.fo * lw;
-  if (tid < T * C::H) {
+  if (tid < T * C::H && !a.wsp) {
     float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
     if ((T * C::H) % 16 == 0 && lw == 16) {
       const float2* g = src + int64_t(tid >> 4) * wb_stride + (tid & 15);
@@ -477,8 +478,20 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
     const int kz = tid % C::H, ky = tid / C::H;
     float2* base = sp + ky * C::SY + kz;
     float2 v[T];
+    if (a.wsp) {
+      // f = 1: Y[w](row, i) = X[w](row) W[w](i) (lw = 16), w = kx*T*H + tid
+      const float2* sx = a.spec + ml * 16;
+      const float2* sw = a.wsp + i * 16;
+      const int64_t xs = a.mstride * 16, ws = a.w_fo * 16;
 #pragma unroll
-    for (int x = 0; x < T; ++x) v[x] = base[x * C::SX];
+      for (int x = 0; x < T; ++x) {
+        const int w = x * T * C::H + tid;
+        v[x] = cmul(__ldg(sx + int64_t(w >> 4) * xs + (w & 15)), __ldg(sw + int64_t(w >> 4) * ws + (w & 15)));
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < T; ++x) v[x] = base[x * C::SX];
+    }
     fft<T, true>(v);
 #pragma unroll
     for (int x = 0; x < T; ++x) base[x * C::SX] = v[x];

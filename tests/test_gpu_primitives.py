@@ -452,19 +452,21 @@ def test_conv_fft_quad_tiles_3xtf32_split(oracle, ctx, monkeypatch, fo):
     assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
 
 
-@pytest.mark.parametrize("T", [24, 32, 40])
-def test_conv_fft_single_input_map_fused_inverse(oracle, ctx, T):
+@pytest.mark.parametrize("T,pair", [(24, True), (32, True), (40, True), (8, False), (16, False),
+                                    (32, False), (36, False)])
+def test_conv_fft_single_input_map_fused_inverse(oracle, ctx, T, pair):
     """f = 1 FFT layers (the first layers of n726/n926) skip the Y spectra: the
-    CTA-pair inverse multiplies each input spectrum line by its output map's
-    kernel spectrum on load.  Against the C oracle, several tiles per axis."""
+    inverse (CTA pair or one CTA) multiplies each input spectrum line by its
+    output map's kernel spectrum on load.  Against the C oracle, several tiles
+    per axis."""
     import paper_1606_05688_b200 as v
-    S, f, fo, k = 2, 1, 16, (7, 6, 5)
+    S, f, fo, k = 2, 1, 16, (min(7, T), min(6, T), min(5, T))
     n = (2 * T + 3, T + 8, 2 * T - 5)
     rng = np.random.default_rng(T + 100)
     x = rng.uniform(-1, 1, (S, f) + n).astype(np.float32)
     w = (rng.uniform(-1, 1, (fo, f) + k) * 0.1).astype(np.float32)
     b = rng.uniform(-0.1, 0.1, fo).astype(np.float32)
-    got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=False, cta_pair=True, ctx=ctx)
+    got = v.conv_fft_tiled(x, v.ConvLayerParams(w, b, "relu"), T, tensor_cores=False, cta_pair=pair, ctx=ctx)
     assert rel_error(got, oracle.conv(x, w, b, True)) <= 1e-4
 
 
