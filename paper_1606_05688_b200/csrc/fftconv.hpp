@@ -49,6 +49,7 @@ struct InvTileArgs {
   // the kernel spectrum of its output map (wsp, [w/16][w_fo][1][16]) on load
   const float2* wsp = nullptr;
   int64_t w_fo = 0;
+  int direct_x = 0;          // one-CTA inverse: x lines loaded from HBM into registers (no staging)
 };
 
 struct GemmArgs {

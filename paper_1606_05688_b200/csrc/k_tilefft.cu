@@ -446,11 +446,11 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
   const int tid = threadIdx.x;
 
   // A: spectrum lines -> smem (asynchronous 8-byte copies); with a single
-  // input map (a.wsp) the x pass forms Y = X W from HBM itself instead
+  // input map (a.wsp) or direct_x the x pass loads from HBM itself instead
   const int lw = a.lw, lshift = __ffs(lw) - 1;
   const float2* src = a.spec + (ml * a.fo + i) * lw;
   const int64_t wb_stride = a.mstride * a.fo * lw;
-  if (tid < T * C::H && !a.wsp) {
+  if (tid < T * C::H && !a.wsp && !a.direct_x) {
     float2* s = sp + (tid / C::H) * C::SY + tid % C::H;
     if ((T * C::H) % 16 == 0 && lw == 16) {
       const float2* g = src + int64_t(tid >> 4) * wb_stride + (tid & 15);
@@ -487,6 +487,14 @@ __global__ void __launch_bounds__(TileCfg<T>::THREADS, TileCfg<T>::MINB)
       for (int x = 0; x < T; ++x) {
         const int w = x * T * C::H + tid;
         v[x] = cmul(__ldg(sx + int64_t(w >> 4) * xs + (w & 15)), __ldg(sw + int64_t(w >> 4) * ws + (w & 15)));
+      }
+    } else if (a.direct_x) {
+      // straight from HBM into registers: no shared-memory round trip
+      int w = tid;
+#pragma unroll
+      for (int x = 0; x < T; ++x) {
+        v[x] = __ldg(src + int64_t(w >> lshift) * wb_stride + (w & (lw - 1)));
+        w += T * C::H;
       }
     } else {
 #pragma unroll
@@ -908,7 +916,16 @@ void launch_tile_fwd(Ctx* c, int T, const FwdTileArgs& a, int64_t nblocks) {
   VXG_TILE_SWITCH(fwd_t)
 }
 
-void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a, int64_t nblocks) {
+void launch_tile_inv(Ctx* c, int T, const InvTileArgs& a0, int64_t nblocks) {
+  // The one-CTA inverse loads its x lines from HBM straight into registers at
+  // T >= 28 (T = 30 / 36: -7 / -9 % inverse time) and stages them through
+  // shared memory below (T = 16: +4 % direct), profiles/r2_experiments.md §17;
+  // VXG_INV_DIRECT=0/1 forces either
+  InvTileArgs a = a0;
+  {
+    const char* e = std::getenv("VXG_INV_DIRECT");
+    a.direct_x = e ? std::strcmp(e, "1") == 0 : T >= 28;
+  }
   const double nw = double(T) * T * (T / 2 + 1);
   KScope ks(c, VXG_K_TILE_INV, 0.0,
             double(nblocks) * (8.0 * nw + 4.0 * double(a.vx) * a.vy * a.vz));

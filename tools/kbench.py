@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--extent", type=int, default=722)
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--k", type=int, default=7)
+    ap.add_argument("--single-only", action="store_true")
     a = ap.parse_args()
     ctx = v.Context(0)
     res = {}
@@ -86,7 +87,7 @@ def main():
         w = (torch.rand((80, 80, kk, kk, kk), device="cuda", generator=g) * 2 - 1) * 0.02
         b = torch.rand((80,), device="cuda", generator=g) * 0.2 - 0.1
         p = v.ConvLayerParams(w, b, "relu")
-        for pair in (False, True):
+        for pair in ((False,) if a.single_only else (False, True)):
             ctx.profile(True)
             t = timed(ctx, lambda: v.conv_fft_tiled(x, p, a.T, tensor_cores=True, cta_pair=pair, ctx=ctx))
             ks = ctx.kernel_stats()
